@@ -1,0 +1,206 @@
+/*
+ * tc.h -- C ABI of libtc, the B200-native tensor-collective hot path of MXNET-MPI
+ *         (arXiv 1801.03855).  PAPER.md line n is cited as P:n, SPEC.md line n as S:n.
+ *
+ * What it computes:
+ *   tc_allreduce    -- the *tensor allreduce* of §6: the T tensors a rank holds are
+ *                      one flat logical vector ("a group of vectors on a node as a single
+ *                      object"), reduced by reduce-scatter + allgather.
+ *   tc_sgd_step     -- that allreduce fused with the SGD update of Eq. 1 with the
+ *                      1/mini_batch "rescale" of Fig. code-snippet-2 and momentum.
+ *   tc_easgd_update -- the elastic-averaging update, Eqs. elastic1/elastic2, in the
+ *                      synchronous sum form  x_i -= a(x_i - xc);  xc += a * sum_i (x_i - xc).
+ *
+ * Data types: fp32 tensors only (the paper never states a precision; fp32 is implied, R19).
+ *
+ * Ownership: the caller owns every tensor.  A tensor passed to tc_group_create must stay
+ * allocated and unmoved until tc_group_destroy returns on all ranks.  libtc owns its flag,
+ * staging and descriptor buffers and its CUDA-IPC mappings.  Streams belong to the caller:
+ * hot-path calls enqueue one kernel on `stream` (a cudaStream_t, NULL = legacy default
+ * stream) and return; completion is stream-ordered.
+ *
+ * Collectives: every call on a comm (create, group create/destroy, the three hot-path calls)
+ * is COLLECTIVE -- every rank of the comm makes the same calls, in the same order, with the
+ * same scalar arguments ("the operations are enqueued in order to avoid deadlocks").
+ * Consecutive hot-path calls on one comm must be stream-ordered on each rank.
+ *
+ * Errors: every function returns a tc_status synchronously; nothing throws across the ABI.
+ * Non-finite *data* is not checked on the hot path (NaN/Inf propagate).
+ */
+#ifndef TC_H_
+#define TC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TC_OK = 0,
+  TC_ERR_INVALID_ARG = 1,     /* null pointer, bad count/size/alignment, bad hyper-parameter   */
+  TC_ERR_SHAPE_MISMATCH = 2,  /* ranks disagree on (T, n_t), or groups not congruent   */
+  TC_ERR_NOT_SHAREABLE = 3,   /* a tensor's allocation cannot be exported with CUDA IPC        */
+  TC_ERR_BUSY = 4,            /* another host thread is inside a call on this comm     */
+  TC_ERR_TIMEOUT = 5,         /* a peer did not arrive at a device barrier (sticky)     */
+  TC_ERR_CUDA = 6,            /* a CUDA runtime call failed                                     */
+  TC_ERR_BOOTSTRAP = 7,       /* the caller's allgather callback failed                         */
+  TC_ERR_UNSUPPORTED = 8      /* e.g. nranks > TC_MAX_RANKS                                      */
+} tc_status;
+
+#define TC_MAX_RANKS 8        /* one NVSwitch box */
+
+#if defined(__GNUC__)
+#define TC_API __attribute__((visibility("default")))
+#else
+#define TC_API
+#endif
+
+typedef struct tc_plan tc_plan;    /* A1 descriptor: flat slot space + owner partition (host) */
+typedef struct tc_comm tc_comm;    /* ranks (GPUs) with peer-mapped flag/staging buffers      */
+typedef struct tc_group tc_group;  /* caller tensors flattened over a comm, peer-mapped        */
+
+/* Bootstrap allgather supplied by the caller (torch.distributed over gloo in the Python
+ * binding).  Gathers `bytes_per_rank` bytes from every rank of the comm into `recv`
+ * (rank-major, nranks * bytes_per_rank bytes).  Returns 0 on success. */
+typedef int (*tc_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes_per_rank);
+
+/* Library version (major*10000 + minor*100 + patch). */
+TC_API int tc_version(void);
+
+/* Human-readable name of a status code (static storage; never NULL). */
+TC_API const char* tc_status_string(tc_status s);
+
+/* ---------------------------------------------------------------------------------------
+ * A1: group descriptor (host only, no CUDA).  P:331 "the buffer from each process is
+ * partitioned into nearly equal parts"; reading R2: 16-byte slots.  Tensor t of n_t fp32
+ * elements occupies ceil(n_t/4) consecutive slots of one flat slot space of M slots (the last
+ * slot of a tensor may be partial).  Rank r owns slots [floor(M*r/p), floor(M*(r+1)/p)).
+ * A segment is a maximal run of slots inside one tensor and one owner (<= T+p-1 of them).
+ * --------------------------------------------------------------------------------------- */
+
+/* Builds the plan for `ntensors` tensors of `numels[t]` elements (numels[t] >= 0) over
+ * `nranks` ranks.  If `ag` is non-NULL the call is collective: every rank's (T, numels) is
+ * checked through `ag` and TC_ERR_SHAPE_MISMATCH is returned on EVERY rank if any differ.
+ * With ag == NULL the plan is local.  Errors: TC_ERR_INVALID_ARG (nranks < 1, rank out of
+ * range, ntensors < 1, numels NULL or negative, M >= 2^31 slots), TC_ERR_UNSUPPORTED
+ * (nranks > TC_MAX_RANKS), TC_ERR_BOOTSTRAP.  *out is owned by the caller (tc_plan_destroy). */
+TC_API tc_status tc_plan_create(int rank, int nranks, int ntensors, const int64_t* numels,
+                         tc_allgather_fn ag, void* ag_ctx, tc_plan** out);
+TC_API void tc_plan_destroy(tc_plan* plan);
+TC_API int64_t tc_plan_num_elements(const tc_plan* plan);              /* N = sum_t n_t            */
+TC_API int64_t tc_plan_num_slots(const tc_plan* plan);                 /* M                        */
+TC_API uint64_t tc_plan_hash(const tc_plan* plan);                     /* congruence hash of (T,n) */
+/* First slot and slot count of tensor t. */
+TC_API tc_status tc_plan_tensor_slots(const tc_plan* plan, int t, int64_t* first_slot, int64_t* nslots);
+/* Owner slot range [lo, hi) of rank r. */
+TC_API tc_status tc_plan_owner_range(const tc_plan* plan, int r, int64_t* lo, int64_t* hi);
+TC_API int tc_plan_num_segments(const tc_plan* plan);
+/* Segment i: tensor index, owner rank, and its global slot range [slot_lo, slot_hi). */
+TC_API tc_status tc_plan_segment(const tc_plan* plan, int i, int* tensor, int* owner,
+                          int64_t* slot_lo, int64_t* slot_hi);
+
+/* ---------------------------------------------------------------------------------------
+ * Communicators.
+ * --------------------------------------------------------------------------------------- */
+
+/* One rank per process (the production layout).  Collective over `nranks` processes; `ag`
+ * is the bootstrap allgather over exactly those processes (rank order = comm rank order).
+ * Allocates the flag and one-shot staging buffers on `cuda_device`, exports them with
+ * cudaIpcGetMemHandle and maps every peer's.  Errors: TC_ERR_INVALID_ARG,
+ * TC_ERR_UNSUPPORTED (nranks > TC_MAX_RANKS), TC_ERR_CUDA, TC_ERR_BOOTSTRAP. */
+TC_API tc_status tc_comm_create(int rank, int nranks, int cuda_device, tc_allgather_fn ag,
+                         void* ag_ctx, tc_comm** out);
+
+/* All `nranks` ranks live in this process on ONE device (test/debug layout): every hot-path
+ * call launches ONE cooperative kernel whose blockIdx.y is the rank, running exactly the
+ * per-rank code and flag protocol of the multi-process layout (peer "mappings" are plain
+ * local pointers).  Not collective. */
+TC_API tc_status tc_comm_create_emulated(int nranks, int cuda_device, tc_comm** out);
+
+/* Launch tuning, must be identical on all ranks.  num_ctas: CTAs per rank for two-shot calls
+ * (0 = automatic: a full wave of the GPU); threads: threads per CTA (0 = 512; a multiple of 32
+ * in [64, 1024]); oneshot_max_bytes: groups of at most this many bytes use the one-shot
+ * algorithm (-1 = automatic, 0 = never; capped by the staging capacity).  Applies to later
+ * calls.  Errors: TC_ERR_INVALID_ARG. */
+TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t oneshot_max_bytes);
+
+/* Device-barrier timeout in milliseconds (default 30000, or env TC_TIMEOUT_MS). */
+TC_API tc_status tc_comm_set_timeout(tc_comm* comm, int64_t timeout_ms);
+
+/* Fault injection for tests (emulated comms only): the CTAs of rank `absent_rank` return
+ * immediately without arriving at any barrier (-1 = off), so the other ranks time out. */
+TC_API tc_status tc_comm_set_debug_absent_rank(tc_comm* comm, int absent_rank);
+
+/* Sticky device-side error: TC_ERR_TIMEOUT once any barrier timed out, else TC_OK.  Reads
+ * host-mapped memory; does not synchronize.  After a timeout the comm must be destroyed. */
+TC_API tc_status tc_comm_async_error(tc_comm* comm);
+
+TC_API int tc_comm_rank(const tc_comm* comm);      /* -1 for an emulated comm */
+TC_API int tc_comm_nranks(const tc_comm* comm);
+
+/* Collective: synchronizes the device, waits for every rank (bootstrap barrier), unmaps and
+ * frees.  All groups of the comm must have been destroyed first (TC_ERR_INVALID_ARG). */
+TC_API tc_status tc_comm_destroy(tc_comm* comm);
+
+/* ---------------------------------------------------------------------------------------
+ * Tensor groups (the paper's "tensor", generalized to T tensors per rank).
+ * --------------------------------------------------------------------------------------- */
+
+/* Collective.  `ptrs[t]` is this rank's device pointer to tensor t (fp32, 4-byte aligned,
+ * contiguous), `numels[t]` its element count (0 allowed, then ptrs[t] may be NULL).  For an
+ * emulated comm `ptrs` holds nranks*ntensors pointers, rank-major (ptrs[r*ntensors + t]).
+ * Nothing is copied: each pointer's cudaMalloc allocation is exported with CUDA IPC and
+ * mapped by every peer (allocations shared by several tensors are mapped once).  Tensors whose
+ * pointers are 16-byte aligned on every rank use 16-byte vector loads; others a scalar path.
+ * Errors: TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH (ranks disagree on T or any n_t; returned
+ * on every rank), TC_ERR_NOT_SHAREABLE (e.g. PyTorch expandable_segments allocations),
+ * TC_ERR_CUDA, TC_ERR_BOOTSTRAP. */
+TC_API tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const int64_t* numels,
+                          tc_group** out);
+
+/* Collective: synchronizes the device, waits for every rank, then unmaps. */
+TC_API tc_status tc_group_destroy(tc_group* group);
+
+/* ---------------------------------------------------------------------------------------
+ * Hot path.  One kernel launch per call on `stream`.
+ * --------------------------------------------------------------------------------------- */
+
+/* A3+A4 (or A5 one-shot for small groups): in place, on every rank,
+ *     x[t][j] := round_fp32( (sum_{k=0..p-1} x_k[t][j]) * scale )
+ * summed in float64 in canonical rank order k = 0..p-1 and rounded once (readings R3, R4), so
+ * the result is bit-identical on every rank and for every algorithm.  Errors:
+ * TC_ERR_INVALID_ARG (NULL group, non-finite scale), TC_ERR_TIMEOUT (sticky), TC_ERR_BUSY,
+ * TC_ERR_CUDA (launch failure). */
+TC_API tc_status tc_allreduce(tc_group* x, float scale, void* stream);
+
+/* A6: gradient allreduce fused with the SGD(-momentum) update, on every rank, per element:
+ *     G   = sum_k g_k                (float64, rank order, rounded once; written back to g)
+ *     t   = (rescale*G) + (wd*w)                        each op rounded to fp32, no FMA
+ *     dw := (momentum*dw) - (lr*t)                      (reading R12; Eq. 1 at momentum=wd=0)
+ *     w  := w + dw                                      (Eq. 1: w_{t+1} = w_t + dw)
+ * w, g, dw must be congruent groups on the same comm (same T and n_t) -- normally w and dw
+ * are replicated, so every rank ends with identical w, dw.  Errors: TC_ERR_INVALID_ARG
+ * (NULL, non-finite hyper-parameter), TC_ERR_SHAPE_MISMATCH, TC_ERR_TIMEOUT, TC_ERR_BUSY,
+ * TC_ERR_CUDA. */
+TC_API tc_status tc_sgd_step(tc_group* w, tc_group* g, tc_group* dw, float lr, float momentum,
+                      float wd, float rescale, void* stream);
+
+/* A7: elastic averaging over a comm with one rank per client (c = nranks), per element:
+ *     d_i  = x_i - xc                     (each client's params vs the replicated center)
+ *     x_i := x_i - alpha*d_i              (Eq. elastic2)
+ *     xc  := xc + alpha*(d_0 + d_1 + ... + d_{c-1})   (Eq. elastic1 summed over clients, R10)
+ * all in fp32 with every op rounded (fp32 mirror), sums in client order.  `center` is
+ * replicated and stays bit-identical on every rank.  alpha in [0, 1].  Errors:
+ * TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_TIMEOUT, TC_ERR_BUSY, TC_ERR_CUDA. */
+TC_API tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream);
+
+/* Introspection of the most recent hot-path launch on this comm (for benchmarks):
+ * algorithm (0 = local p=1, 1 = two-shot, 2 = one-shot), grid CTAs per rank, threads. */
+TC_API tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TC_H_ */

@@ -1,0 +1,127 @@
+// Internal structures of libtc shared by the host runtime (tc_runtime.cu) and the kernels
+// (tc_kernels.cu).  Not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <vector>
+#include <map>
+#include <atomic>
+#include <string>
+#include <array>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tc.h"
+
+namespace tc {
+
+constexpr int kMaxRanks = TC_MAX_RANKS;
+constexpr int kMaxCtas = 1024;                 // per barrier and source rank
+constexpr int kNumBarriers = 3;                // entry, mid, exit
+constexpr size_t kFlagWords = (size_t)kNumBarriers * kMaxRanks * kMaxCtas;
+constexpr size_t kStageCapacity = 8u << 20;    // one-shot staging bytes per parity
+constexpr int64_t kDefaultOneshotMax = 256 << 10;
+
+enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
+enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
+enum Algo { ALGO_LOCAL = 0, ALGO_TWOSHOT = 1, ALGO_ONESHOT = 2 };
+
+// ---------------------------------------------------------------- A1 descriptor (host)
+struct Plan {
+  int rank = 0, nranks = 1, T = 0;
+  std::vector<int64_t> numel;        // [T]
+  std::vector<int64_t> slot_prefix;  // [T+1]
+  int64_t N = 0, M = 0;
+  uint64_t hash = 0;
+  struct Segment { int tensor, owner; int64_t lo, hi; };
+  std::vector<Segment> segments;
+  int64_t owner_lo(int r) const { return M * r / nranks; }
+  int64_t owner_hi(int r) const { return M * (r + 1) / nranks; }
+};
+
+tc_status build_plan(int rank, int nranks, int ntensors, const int64_t* numels, Plan& out);
+uint64_t plan_hash(int ntensors, const int64_t* numels);
+// Collective allgather through the caller's callback; returns TC_ERR_BOOTSTRAP on failure.
+tc_status bootstrap_allgather(tc_allgather_fn ag, void* ctx, int nranks, const void* send,
+                              void* recv, size_t bytes);
+
+// ---------------------------------------------------------------- kernel parameters
+// Passed by value to every hot-path kernel.  Tables are device arrays.
+struct KParams {
+  int p;                 // ranks in the comm
+  int rank0;             // comm rank of blockIdx.y == 0
+  int T;
+  int M;                 // total 16-B slots
+  const int* prefix;     // [T+1] slot prefix
+  const int64_t* numel;  // [T]
+  const uint8_t* vec_ok; // [T] primary group 16-B aligned on every rank
+  const uint8_t* vec_ok_b; // [T] same for group b (nullptr if unused)
+  const uint8_t* vec_ok_c; // [T] same for group c (nullptr if unused)
+  float* const* a;       // [p*T] primary group: x (allreduce, easgd) or g (sgd)
+  float* const* b;       // [p*T] w (sgd) or center (easgd)
+  float* const* c;       // [p*T] dw (sgd)
+  uint32_t* const* flags;// [p] flag buffers (peer-mapped)
+  float* const* stage;   // [p] one-shot staging buffers (peer-mapped), parity-selected
+  uint32_t epoch;
+  int stage_off;         // float offset of this call's parity half
+  float scale, lr, mu, wd, rescale, alpha;
+  unsigned long long timeout_ns;
+  int* err;              // host-mapped sticky error word
+  int absent_rank;       // fault injection (emulated only), -1 off
+};
+
+// Kernel launchers (tc_kernels.cu).
+cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int threads, int nlocal,
+                       bool cooperative, cudaStream_t stream);
+int max_ctas_per_sm(int op, int algo, int p, int threads);
+
+// ---------------------------------------------------------------- runtime objects
+struct MappedBase {
+  void* ptr = nullptr;
+  int refs = 0;
+};
+
+struct Comm {
+  int rank = 0;            // -1 when emulated
+  int nranks = 1;
+  bool emulated = false;
+  int device = 0;
+  int num_sms = 148;
+  tc_allgather_fn ag = nullptr;
+  void* ag_ctx = nullptr;
+  // per-rank buffers: own (index = rank) allocated here, peers IPC-mapped.
+  std::array<uint32_t*, kMaxRanks> flags{};
+  std::array<float*, kMaxRanks> stage{};
+  uint32_t** d_flags = nullptr;   // device table [p]
+  float** d_stage = nullptr;      // device table [p]
+  int* h_err = nullptr;           // host-mapped
+  int* d_err = nullptr;
+  uint32_t epoch = 0;
+  int tune_ctas = 0, tune_threads = 512;
+  int64_t tune_oneshot = -1;
+  unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;
+  int absent_rank = -1;
+  int last_algo = -1, last_ctas = 0, last_threads = 0;
+  std::atomic<bool> busy{false};
+  int live_groups = 0;
+  // IPC mapping cache: (peer, handle bytes) -> mapping
+  std::map<std::pair<int, std::string>, MappedBase> ipc_cache;
+};
+
+struct Group {
+  Comm* comm = nullptr;
+  Plan plan;
+  std::vector<float*> h_ptrs;    // [p*T] (peer-mapped pointers for real comms)
+  float** d_ptrs = nullptr;      // device copy
+  int* d_prefix = nullptr;
+  int64_t* d_numel = nullptr;
+  uint8_t* d_vec_ok = nullptr;
+  std::vector<std::pair<int, std::string>> mapped_keys;  // ipc_cache keys held
+};
+
+}  // namespace tc
+
+struct tc_plan { tc::Plan p; };
+struct tc_comm { tc::Comm c; };
+struct tc_group { tc::Group g; };

@@ -1,0 +1,614 @@
+// libtc host runtime: communicators, CUDA-IPC peer mapping of caller tensors (no copies), the
+// hot-path entry points of include/tc.h and their argument checking.
+//
+// The only cross-process traffic happens at create/destroy time through the caller's bootstrap
+// allgather ("all the workers call MPI_Init()" -- here torch.distributed/gloo).  A
+// hot-path call is host validation + ONE kernel launch on the caller's stream.
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "tc_internal.h"
+
+using namespace tc;
+
+namespace {
+
+// cuMemGetAddressRange through the runtime's driver entry point (libcuda is not linked, so the
+// library also loads on machines without a driver -- the CPU test box).
+typedef int (*PFN_addr_range)(unsigned long long*, size_t*, unsigned long long);
+
+cudaError_t alloc_base(const void* p, void** base) {
+  static PFN_addr_range fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !f) return cudaErrorNotSupported;
+    fn = (PFN_addr_range)f;
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)(uintptr_t)p) != 0) return cudaErrorInvalidValue;
+  *base = (void*)(uintptr_t)b;
+  return cudaSuccess;
+}
+
+#define TC_CUDA(expr)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      if (std::getenv("TC_DEBUG"))                                                          \
+        std::fprintf(stderr, "libtc: %s failed: %s (%s:%d)\n", #expr, cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                                   \
+      return TC_ERR_CUDA;                                                                   \
+    }                                                                                       \
+  } while (0)
+
+struct BusyGuard {
+  std::atomic<bool>& f;
+  bool ok;
+  explicit BusyGuard(std::atomic<bool>& b) : f(b) { ok = !f.exchange(true); }
+  ~BusyGuard() {
+    if (ok) f.store(false);
+  }
+};
+
+unsigned long long env_timeout_ns() {
+  const char* s = std::getenv("TC_TIMEOUT_MS");
+  long long ms = s ? std::atoll(s) : 30000;
+  if (ms <= 0) ms = 30000;
+  return (unsigned long long)ms * 1000000ull;
+}
+
+tc_status alloc_comm_buffers(Comm& c, int r) {
+  TC_CUDA(cudaMalloc((void**)&c.flags[r], kFlagWords * sizeof(uint32_t)));
+  TC_CUDA(cudaMemset(c.flags[r], 0, kFlagWords * sizeof(uint32_t)));
+  TC_CUDA(cudaMalloc((void**)&c.stage[r], 2 * kStageCapacity));
+  return TC_OK;
+}
+
+tc_status finish_comm(Comm& c) {
+  TC_CUDA(cudaHostAlloc((void**)&c.h_err, sizeof(int), cudaHostAllocMapped));
+  *c.h_err = 0;
+  TC_CUDA(cudaHostGetDevicePointer((void**)&c.d_err, c.h_err, 0));
+  TC_CUDA(cudaMalloc((void**)&c.d_flags, sizeof(uint32_t*) * kMaxRanks));
+  TC_CUDA(cudaMalloc((void**)&c.d_stage, sizeof(float*) * kMaxRanks));
+  TC_CUDA(cudaMemcpy(c.d_flags, c.flags.data(), sizeof(uint32_t*) * kMaxRanks,
+                     cudaMemcpyHostToDevice));
+  TC_CUDA(cudaMemcpy(c.d_stage, c.stage.data(), sizeof(float*) * kMaxRanks,
+                     cudaMemcpyHostToDevice));
+  int sms = 0;
+  TC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+  c.num_sms = sms;
+  c.timeout_ns = env_timeout_ns();
+  return TC_OK;
+}
+
+// Map (or reuse) peer `peer`'s allocation exported as `h`.
+tc_status map_peer(Comm& c, int peer, const cudaIpcMemHandle_t& h, void** out,
+                   std::pair<int, std::string>* key_out) {
+  std::pair<int, std::string> key(peer, std::string(h.reserved, sizeof(h.reserved)));
+  auto it = c.ipc_cache.find(key);
+  if (it == c.ipc_cache.end()) {
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      if (std::getenv("TC_DEBUG"))
+        std::fprintf(stderr, "libtc: cudaIpcOpenMemHandle(peer %d): %s\n", peer,
+                     cudaGetErrorString(e));
+      return TC_ERR_CUDA;
+    }
+    it = c.ipc_cache.emplace(key, MappedBase{p, 0}).first;
+  }
+  it->second.refs++;
+  *out = it->second.ptr;
+  if (key_out) *key_out = key;
+  return TC_OK;
+}
+
+void unmap_peer(Comm& c, const std::pair<int, std::string>& key) {
+  auto it = c.ipc_cache.find(key);
+  if (it == c.ipc_cache.end()) return;
+  if (--it->second.refs == 0) {
+    cudaIpcCloseMemHandle(it->second.ptr);
+    c.ipc_cache.erase(it);
+  }
+}
+
+tc_status comm_barrier(Comm& c) {
+  if (c.emulated || c.nranks == 1) return TC_OK;
+  int32_t one = 1, all[kMaxRanks];
+  return bootstrap_allgather(c.ag, c.ag_ctx, c.nranks, &one, all, sizeof(one));
+}
+
+// Collective status agreement: every rank learns the worst status of all ranks.
+tc_status agree(Comm& c, tc_status mine) {
+  if (c.emulated || c.nranks == 1) return mine;
+  int32_t s = (int32_t)mine, all[kMaxRanks];
+  tc_status bs = bootstrap_allgather(c.ag, c.ag_ctx, c.nranks, &s, all, sizeof(s));
+  if (bs != TC_OK) return bs;
+  for (int r = 0; r < c.nranks; ++r)
+    if (all[r] != TC_OK) return (tc_status)all[r];
+  return TC_OK;
+}
+
+void free_group_device(Group& g) {
+  cudaFree(g.d_ptrs);
+  cudaFree(g.d_prefix);
+  cudaFree(g.d_numel);
+  cudaFree(g.d_vec_ok);
+  g.d_ptrs = nullptr;
+  g.d_prefix = nullptr;
+  g.d_numel = nullptr;
+  g.d_vec_ok = nullptr;
+}
+
+tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
+  const Plan& pl = g.plan;
+  std::vector<int> prefix(pl.slot_prefix.begin(), pl.slot_prefix.end());
+  TC_CUDA(cudaMalloc((void**)&g.d_ptrs, sizeof(float*) * g.h_ptrs.size()));
+  TC_CUDA(cudaMalloc((void**)&g.d_prefix, sizeof(int) * prefix.size()));
+  TC_CUDA(cudaMalloc((void**)&g.d_numel, sizeof(int64_t) * pl.numel.size()));
+  TC_CUDA(cudaMalloc((void**)&g.d_vec_ok, vec_ok.size()));
+  TC_CUDA(cudaMemcpy(g.d_ptrs, g.h_ptrs.data(), sizeof(float*) * g.h_ptrs.size(),
+                     cudaMemcpyHostToDevice));
+  TC_CUDA(cudaMemcpy(g.d_prefix, prefix.data(), sizeof(int) * prefix.size(),
+                     cudaMemcpyHostToDevice));
+  TC_CUDA(cudaMemcpy(g.d_numel, pl.numel.data(), sizeof(int64_t) * pl.numel.size(),
+                     cudaMemcpyHostToDevice));
+  TC_CUDA(cudaMemcpy(g.d_vec_ok, vec_ok.data(), vec_ok.size(), cudaMemcpyHostToDevice));
+  return TC_OK;
+}
+
+bool finite(float v) { return std::isfinite(v); }
+
+// ------------------------------------------------------------------ hot-path dispatcher
+tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr, float mu,
+                  float wd, float rescale, float alpha, cudaStream_t stream) {
+  Comm& c = *ga->comm;
+  BusyGuard busy(c.busy);
+  if (!busy.ok) return TC_ERR_BUSY;
+  if (*(volatile int*)c.h_err) return (tc_status)*(volatile int*)c.h_err;
+  const Plan& pl = ga->plan;
+  const int p = c.nranks;
+  if (pl.M == 0) return TC_OK;  // empty group: nothing to reduce (still collective-safe)
+  KParams kp;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.p = p;
+  kp.rank0 = c.emulated ? 0 : c.rank;
+  kp.T = pl.T;
+  kp.M = (int)pl.M;
+  kp.prefix = ga->d_prefix;
+  kp.numel = ga->d_numel;
+  kp.vec_ok = ga->d_vec_ok;
+  kp.a = ga->d_ptrs;
+  kp.b = gb ? gb->d_ptrs : nullptr;
+  kp.c = gc ? gc->d_ptrs : nullptr;
+  kp.flags = c.d_flags;
+  kp.stage = c.d_stage;
+  kp.scale = scale;
+  kp.lr = lr;
+  kp.mu = mu;
+  kp.wd = wd;
+  kp.rescale = rescale;
+  kp.alpha = alpha;
+  kp.timeout_ns = c.timeout_ns;
+  kp.err = c.d_err;
+  kp.absent_rank = c.emulated ? c.absent_rank : -1;
+  // The vector path is taken for a tensor only if it is 16-B aligned in every group involved.
+  kp.vec_ok_b = gb ? gb->d_vec_ok : nullptr;
+  kp.vec_ok_c = gc ? gc->d_vec_ok : nullptr;
+
+  const int threads = c.tune_threads;
+  const int64_t bytes = pl.M * 16;
+  int algo;
+  if (p == 1) {
+    algo = ALGO_LOCAL;
+  } else {
+    int64_t lim = c.tune_oneshot < 0 ? kDefaultOneshotMax : c.tune_oneshot;
+    if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
+    algo = bytes <= lim ? ALGO_ONESHOT : ALGO_TWOSHOT;
+  }
+  const int nlocal = c.emulated ? p : 1;
+  int occ = max_ctas_per_sm(op, algo, p, threads);
+  if (occ < 1) return TC_ERR_CUDA;
+  int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
+  if (cap < 1) cap = 1;
+  int64_t work_slots = (algo == ALGO_TWOSHOT) ? (pl.M + p - 1) / p : pl.M;
+  int64_t want = (work_slots + threads - 1) / threads;
+  int ctas;
+  if (algo == ALGO_LOCAL) {
+    ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * occ);
+  } else if (algo == ALGO_TWOSHOT && c.tune_ctas > 0) {
+    ctas = c.tune_ctas;
+  } else {
+    ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * (algo == ALGO_ONESHOT ? 1 : occ));
+  }
+  if (algo != ALGO_LOCAL) {
+    if (ctas > kMaxCtas) ctas = kMaxCtas;
+    if (ctas > cap) ctas = cap;
+  }
+  if (ctas < 1) ctas = 1;
+  kp.epoch = ++c.epoch;
+  kp.stage_off = (int)((kp.epoch & 1u) * (kStageCapacity / sizeof(float)));
+  cudaError_t e = launch_hot(op, algo, kp, ctas, threads, nlocal, c.emulated && p > 1, stream);
+  if (e != cudaSuccess) {
+    if (std::getenv("TC_DEBUG"))
+      std::fprintf(stderr, "libtc: launch failed: %s\n", cudaGetErrorString(e));
+    return TC_ERR_CUDA;
+  }
+  c.last_algo = algo;
+  c.last_ctas = ctas;
+  c.last_threads = threads;
+  return TC_OK;
+}
+
+bool congruent(const Group* a, const Group* b) {
+  return a->comm == b->comm && a->plan.T == b->plan.T && a->plan.hash == b->plan.hash &&
+         a->plan.numel == b->plan.numel;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tc_version(void) { return 100; }
+
+const char* tc_status_string(tc_status s) {
+  switch (s) {
+    case TC_OK: return "TC_OK";
+    case TC_ERR_INVALID_ARG: return "TC_ERR_INVALID_ARG";
+    case TC_ERR_SHAPE_MISMATCH: return "TC_ERR_SHAPE_MISMATCH";
+    case TC_ERR_NOT_SHAREABLE: return "TC_ERR_NOT_SHAREABLE";
+    case TC_ERR_BUSY: return "TC_ERR_BUSY";
+    case TC_ERR_TIMEOUT: return "TC_ERR_TIMEOUT";
+    case TC_ERR_CUDA: return "TC_ERR_CUDA";
+    case TC_ERR_BOOTSTRAP: return "TC_ERR_BOOTSTRAP";
+    case TC_ERR_UNSUPPORTED: return "TC_ERR_UNSUPPORTED";
+  }
+  return "TC_ERR_UNKNOWN";
+}
+
+tc_status tc_comm_create(int rank, int nranks, int cuda_device, tc_allgather_fn ag, void* ag_ctx,
+                         tc_comm** out) {
+  if (!out) return TC_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || cuda_device < 0) return TC_ERR_INVALID_ARG;
+  if (nranks > kMaxRanks) return TC_ERR_UNSUPPORTED;
+  if (nranks > 1 && !ag) return TC_ERR_INVALID_ARG;
+  TC_CUDA(cudaSetDevice(cuda_device));
+  tc_comm* h = new tc_comm;
+  Comm& c = h->c;
+  c.rank = rank;
+  c.nranks = nranks;
+  c.device = cuda_device;
+  c.ag = ag;
+  c.ag_ctx = ag_ctx;
+  tc_status st = alloc_comm_buffers(c, rank);
+  struct Hello {
+    int32_t status;
+    int32_t sms;
+    cudaIpcMemHandle_t hflags, hstage;
+  } mine{}, all[kMaxRanks];
+  mine.status = st;
+  if (st == TC_OK && nranks > 1) {
+    if (cudaIpcGetMemHandle(&mine.hflags, c.flags[rank]) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.hstage, c.stage[rank]) != cudaSuccess)
+      mine.status = TC_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&mine.sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  st = bootstrap_allgather(ag, ag_ctx, nranks, &mine, all, sizeof(Hello));
+  if (st == TC_OK)
+    for (int r = 0; r < nranks; ++r)
+      if (all[r].status != TC_OK) st = (tc_status)all[r].status;
+  if (st == TC_OK) {
+    for (int r = 0; r < nranks && st == TC_OK; ++r) {
+      if (r == rank) continue;
+      void* pf = nullptr;
+      void* ps = nullptr;
+      st = map_peer(c, r, all[r].hflags, &pf, nullptr);
+      if (st == TC_OK) st = map_peer(c, r, all[r].hstage, &ps, nullptr);
+      c.flags[r] = (uint32_t*)pf;
+      c.stage[r] = (float*)ps;
+    }
+    st = agree(c, st);
+  }
+  if (st == TC_OK) st = finish_comm(c);
+  if (st == TC_OK) {
+    int min_sms = all[0].sms;
+    for (int r = 1; r < nranks; ++r) min_sms = std::min(min_sms, (int)all[r].sms);
+    c.num_sms = min_sms;  // identical grid on every rank (per-CTA barrier pairing)
+    *out = h;
+    return TC_OK;
+  }
+  for (auto& kv : c.ipc_cache) cudaIpcCloseMemHandle(kv.second.ptr);
+  cudaFree(c.flags[rank]);
+  cudaFree(c.stage[rank]);
+  delete h;
+  return st;
+}
+
+tc_status tc_comm_create_emulated(int nranks, int cuda_device, tc_comm** out) {
+  if (!out) return TC_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (nranks < 1 || cuda_device < 0) return TC_ERR_INVALID_ARG;
+  if (nranks > kMaxRanks) return TC_ERR_UNSUPPORTED;
+  TC_CUDA(cudaSetDevice(cuda_device));
+  tc_comm* h = new tc_comm;
+  Comm& c = h->c;
+  c.rank = -1;
+  c.nranks = nranks;
+  c.emulated = true;
+  c.device = cuda_device;
+  tc_status st = TC_OK;
+  for (int r = 0; r < nranks && st == TC_OK; ++r) st = alloc_comm_buffers(c, r);
+  if (st == TC_OK) st = finish_comm(c);
+  if (st != TC_OK) {
+    for (int r = 0; r < nranks; ++r) {
+      cudaFree(c.flags[r]);
+      cudaFree(c.stage[r]);
+    }
+    delete h;
+    return st;
+  }
+  *out = h;
+  return TC_OK;
+}
+
+tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t oneshot_max) {
+  if (!comm) return TC_ERR_INVALID_ARG;
+  if (num_ctas < 0 || num_ctas > kMaxCtas) return TC_ERR_INVALID_ARG;
+  if (threads != 0 && (threads < 64 || threads > 512 || threads % 32)) return TC_ERR_INVALID_ARG;
+  if (oneshot_max < -1) return TC_ERR_INVALID_ARG;
+  comm->c.tune_ctas = num_ctas;
+  comm->c.tune_threads = threads ? threads : 512;
+  comm->c.tune_oneshot = oneshot_max;
+  return TC_OK;
+}
+
+tc_status tc_comm_set_timeout(tc_comm* comm, int64_t timeout_ms) {
+  if (!comm || timeout_ms <= 0) return TC_ERR_INVALID_ARG;
+  comm->c.timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
+  return TC_OK;
+}
+
+tc_status tc_comm_set_debug_absent_rank(tc_comm* comm, int absent_rank) {
+  if (!comm || !comm->c.emulated || absent_rank < -1 || absent_rank >= comm->c.nranks)
+    return TC_ERR_INVALID_ARG;
+  comm->c.absent_rank = absent_rank;
+  return TC_OK;
+}
+
+tc_status tc_comm_async_error(tc_comm* comm) {
+  if (!comm) return TC_ERR_INVALID_ARG;
+  return (tc_status) * (volatile int*)comm->c.h_err;
+}
+
+int tc_comm_rank(const tc_comm* comm) { return comm ? comm->c.rank : -1; }
+int tc_comm_nranks(const tc_comm* comm) { return comm ? comm->c.nranks : -1; }
+
+tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads) {
+  if (!comm || !algo || !ctas || !threads) return TC_ERR_INVALID_ARG;
+  *algo = comm->c.last_algo;
+  *ctas = comm->c.last_ctas;
+  *threads = comm->c.last_threads;
+  return TC_OK;
+}
+
+tc_status tc_comm_destroy(tc_comm* comm) {
+  if (!comm) return TC_ERR_INVALID_ARG;
+  Comm& c = comm->c;
+  if (c.live_groups != 0) return TC_ERR_INVALID_ARG;
+  cudaSetDevice(c.device);
+  cudaDeviceSynchronize();
+  tc_status st = comm_barrier(c);
+  for (auto& kv : c.ipc_cache) cudaIpcCloseMemHandle(kv.second.ptr);
+  c.ipc_cache.clear();
+  for (int r = 0; r < c.nranks; ++r) {
+    if (c.emulated || r == c.rank) {
+      cudaFree(c.flags[r]);
+      cudaFree(c.stage[r]);
+    }
+  }
+  cudaFree(c.d_flags);
+  cudaFree(c.d_stage);
+  cudaFreeHost(c.h_err);
+  delete comm;
+  return st;
+}
+
+tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const int64_t* numels,
+                          tc_group** out) {
+  if (!out) return TC_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!comm) return TC_ERR_INVALID_ARG;
+  Comm& c = comm->c;
+  const int p = c.nranks;
+  const int myrank = c.emulated ? 0 : c.rank;
+  Plan plan;
+  tc_status st = build_plan(myrank, p, ntensors, numels, plan);
+  const int nlocal = c.emulated ? p : 1;
+  if (st == TC_OK && !ptrs) st = TC_ERR_INVALID_ARG;
+  if (st == TC_OK) {
+    for (int l = 0; l < nlocal && st == TC_OK; ++l)
+      for (int t = 0; t < ntensors; ++t) {
+        const void* q = ptrs[(size_t)l * ntensors + t];
+        if (numels[t] > 0 && (q == nullptr || ((uintptr_t)q & 3u))) {
+          st = TC_ERR_INVALID_ARG;
+          break;
+        }
+      }
+  }
+  cudaSetDevice(c.device);
+
+  // Header exchange: status, T, hash, number of distinct allocations (real comms).
+  std::vector<void*> bases;
+  std::vector<int32_t> base_idx(st == TC_OK ? ntensors : 0, -1);
+  std::vector<int64_t> offs(st == TC_OK ? ntensors : 0, 0);
+  std::vector<cudaIpcMemHandle_t> handles;
+  if (st == TC_OK && !c.emulated && p > 1) {
+    for (int t = 0; t < ntensors && st == TC_OK; ++t) {
+      if (numels[t] == 0) continue;
+      void* base = nullptr;
+      if (alloc_base(ptrs[t], &base) != cudaSuccess) {
+        st = TC_ERR_NOT_SHAREABLE;
+        break;
+      }
+      int idx = -1;
+      for (size_t i = 0; i < bases.size(); ++i)
+        if (bases[i] == base) idx = (int)i;
+      if (idx < 0) {
+        cudaIpcMemHandle_t h;
+        if (cudaIpcGetMemHandle(&h, base) != cudaSuccess) {
+          cudaGetLastError();
+          st = TC_ERR_NOT_SHAREABLE;
+          break;
+        }
+        idx = (int)bases.size();
+        bases.push_back(base);
+        handles.push_back(h);
+      }
+      base_idx[t] = idx;
+      offs[t] = (int64_t)((const char*)ptrs[t] - (const char*)base);
+    }
+  }
+  struct Hdr { int32_t status, T; uint64_t hash; int32_t nbases, pad; } mine{}, all[kMaxRanks];
+  mine.status = st;
+  mine.T = ntensors;
+  mine.hash = st == TC_OK ? plan.hash : 0;
+  mine.nbases = (int32_t)bases.size();
+  if (!c.emulated && p > 1) {
+    tc_status bs = bootstrap_allgather(c.ag, c.ag_ctx, p, &mine, all, sizeof(Hdr));
+    if (bs != TC_OK) return bs;
+    for (int r = 0; r < p; ++r)
+      if (all[r].status != TC_OK) return (tc_status)all[r].status;
+    for (int r = 0; r < p; ++r)
+      if (all[r].T != all[0].T || all[r].hash != all[0].hash) return TC_ERR_SHAPE_MISMATCH;
+  } else if (st != TC_OK) {
+    return st;
+  }
+
+  tc_group* h = new tc_group;
+  Group& g = h->g;
+  g.comm = &c;
+  g.plan = std::move(plan);
+  const int T = ntensors;
+  g.h_ptrs.assign((size_t)p * T, nullptr);
+  std::vector<uint8_t> vec_ok((size_t)T, 1);
+
+  if (c.emulated || p == 1) {
+    for (int l = 0; l < nlocal; ++l)
+      for (int t = 0; t < T; ++t) {
+        float* q = (float*)ptrs[(size_t)l * T + t];
+        g.h_ptrs[(size_t)l * T + t] = q;
+        if (((uintptr_t)q & 15u) != 0) vec_ok[t] = 0;
+      }
+  } else {
+    // Payload exchange: handles, per-tensor (base index, offset), alignment bits.
+    int maxb = 0;
+    for (int r = 0; r < p; ++r) maxb = std::max(maxb, (int)all[r].nbases);
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    const size_t bytes = (size_t)maxb * hb + (size_t)T * (sizeof(int32_t) + sizeof(int64_t) + 1);
+    std::vector<char> send(bytes, 0), recv(bytes * p);
+    char* w = send.data();
+    for (size_t i = 0; i < handles.size(); ++i) std::memcpy(w + i * hb, &handles[i], hb);
+    w += (size_t)maxb * hb;
+    std::memcpy(w, base_idx.data(), sizeof(int32_t) * T);
+    w += sizeof(int32_t) * T;
+    std::memcpy(w, offs.data(), sizeof(int64_t) * T);
+    w += sizeof(int64_t) * T;
+    for (int t = 0; t < T; ++t) w[t] = ((uintptr_t)ptrs[t] & 15u) == 0;
+    st = bootstrap_allgather(c.ag, c.ag_ctx, p, send.data(), recv.data(), bytes);
+    if (st != TC_OK) {
+      delete h;
+      return st;
+    }
+    for (int r = 0; r < p && st == TC_OK; ++r) {
+      const char* rd = recv.data() + (size_t)r * bytes;
+      const int32_t* bi = (const int32_t*)(rd + (size_t)maxb * hb);
+      int64_t off_r[1];
+      const char* offp = rd + (size_t)maxb * hb + sizeof(int32_t) * T;
+      const char* al = offp + sizeof(int64_t) * T;
+      std::vector<void*> rbases(all[r].nbases, nullptr);
+      if (r != c.rank) {
+        for (int i = 0; i < all[r].nbases && st == TC_OK; ++i) {
+          cudaIpcMemHandle_t hh;
+          std::memcpy(&hh, rd + (size_t)i * hb, hb);
+          std::pair<int, std::string> key;
+          st = map_peer(c, r, hh, &rbases[i], &key);
+          if (st == TC_OK) g.mapped_keys.push_back(key);
+        }
+      }
+      for (int t = 0; t < T && st == TC_OK; ++t) {
+        if (!al[t]) vec_ok[t] = 0;
+        if (numels[t] == 0) continue;
+        if (r == c.rank) {
+          g.h_ptrs[(size_t)r * T + t] = (float*)ptrs[t];
+        } else {
+          std::memcpy(off_r, offp + sizeof(int64_t) * t, sizeof(int64_t));
+          g.h_ptrs[(size_t)r * T + t] = (float*)((char*)rbases[bi[t]] + off_r[0]);
+        }
+      }
+    }
+    st = agree(c, st);
+    if (st != TC_OK) {
+      for (auto& k : g.mapped_keys) unmap_peer(c, k);
+      delete h;
+      return st;
+    }
+  }
+  st = upload_group(g, vec_ok);
+  if (!c.emulated && p > 1) st = agree(c, st);
+  if (st != TC_OK) {
+    free_group_device(g);
+    for (auto& k : g.mapped_keys) unmap_peer(c, k);
+    delete h;
+    return st;
+  }
+  c.live_groups++;
+  *out = h;
+  return TC_OK;
+}
+
+tc_status tc_group_destroy(tc_group* group) {
+  if (!group) return TC_ERR_INVALID_ARG;
+  Group& g = group->g;
+  Comm& c = *g.comm;
+  cudaSetDevice(c.device);
+  cudaDeviceSynchronize();
+  tc_status st = comm_barrier(c);  // no peer kernel can still read our tensors
+  for (auto& k : g.mapped_keys) unmap_peer(c, k);
+  free_group_device(g);
+  c.live_groups--;
+  delete group;
+  return st;
+}
+
+tc_status tc_allreduce(tc_group* x, float scale, void* stream) {
+  if (!x || !finite(scale)) return TC_ERR_INVALID_ARG;
+  return run_hot(OP_ALLREDUCE, &x->g, nullptr, nullptr, scale, 0, 0, 0, 0, 0,
+                 (cudaStream_t)stream);
+}
+
+tc_status tc_sgd_step(tc_group* w, tc_group* g, tc_group* dw, float lr, float momentum, float wd,
+                      float rescale, void* stream) {
+  if (!w || !g || !dw) return TC_ERR_INVALID_ARG;
+  if (!finite(lr) || !finite(momentum) || !finite(wd) || !finite(rescale))
+    return TC_ERR_INVALID_ARG;
+  if (!congruent(&g->g, &w->g) || !congruent(&g->g, &dw->g)) return TC_ERR_SHAPE_MISMATCH;
+  return run_hot(OP_SGD, &g->g, &w->g, &dw->g, 1.0f, lr, momentum, wd, rescale, 0,
+                 (cudaStream_t)stream);
+}
+
+tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream) {
+  if (!x || !center || !finite(alpha) || alpha < 0.f || alpha > 1.f) return TC_ERR_INVALID_ARG;
+  if (!congruent(&x->g, &center->g)) return TC_ERR_SHAPE_MISMATCH;
+  return run_hot(OP_EASGD, &x->g, &center->g, nullptr, 1.0f, 0, 0, 0, 0, alpha,
+                 (cudaStream_t)stream);
+}
+
+}  // extern "C"

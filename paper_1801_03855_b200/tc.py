@@ -1,0 +1,322 @@
+"""Thin Python binding of libtc (include/tc.h) -- argument marshalling only.
+
+Every step of the hot path runs in libtc's CUDA kernels; PyTorch supplies device memory, the
+current stream and the torch.distributed (gloo) allgather used to bootstrap a communicator.
+There is no CPU fallback: if libtc.so is missing this module raises on import.
+
+    comm  = Comm.from_process_group()              # one rank per process (torchrun)
+    comm  = Comm.emulated(4, device=0)             # 4 ranks in this process on one GPU (tests)
+    g     = Group(comm, grads)                     # list of fp32 CUDA tensors (no copy)
+    allreduce(g)                                   # x := sum over ranks, in place
+    sgd_step(w, g, dw, lr=0.1, momentum=0.9, wd=1e-4, rescale=1/256)
+    easgd_update(x, center, alpha=0.1)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TC_LIB", os.path.join(_HERE, "libtc.so"))
+
+STATUS = {
+    0: "TC_OK", 1: "TC_ERR_INVALID_ARG", 2: "TC_ERR_SHAPE_MISMATCH", 3: "TC_ERR_NOT_SHAREABLE",
+    4: "TC_ERR_BUSY", 5: "TC_ERR_TIMEOUT", 6: "TC_ERR_CUDA", 7: "TC_ERR_BOOTSTRAP",
+    8: "TC_ERR_UNSUPPORTED",
+}
+TC_OK, TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_NOT_SHAREABLE = 0, 1, 2, 3
+TC_ERR_BUSY, TC_ERR_TIMEOUT, TC_ERR_CUDA, TC_ERR_BOOTSTRAP, TC_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
+ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot"}
+
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_size_t)
+
+_c_int, _c_int64, _c_float, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
+_pp = ctypes.POINTER(ctypes.c_void_p)
+_SIGS = {
+    "tc_version": (_c_int, []),
+    "tc_status_string": (ctypes.c_char_p, [_c_int]),
+    "tc_plan_create": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_int64), ALLGATHER_FN,
+                                _vp, _pp]),
+    "tc_plan_destroy": (None, [_vp]),
+    "tc_plan_num_elements": (_c_int64, [_vp]),
+    "tc_plan_num_slots": (_c_int64, [_vp]),
+    "tc_plan_hash": (ctypes.c_uint64, [_vp]),
+    "tc_plan_tensor_slots": (_c_int, [_vp, _c_int, ctypes.POINTER(_c_int64),
+                                      ctypes.POINTER(_c_int64)]),
+    "tc_plan_owner_range": (_c_int, [_vp, _c_int, ctypes.POINTER(_c_int64),
+                                     ctypes.POINTER(_c_int64)]),
+    "tc_plan_num_segments": (_c_int, [_vp]),
+    "tc_plan_segment": (_c_int, [_vp, _c_int, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int),
+                                 ctypes.POINTER(_c_int64), ctypes.POINTER(_c_int64)]),
+    "tc_comm_create": (_c_int, [_c_int, _c_int, _c_int, ALLGATHER_FN, _vp, _pp]),
+    "tc_comm_create_emulated": (_c_int, [_c_int, _c_int, _pp]),
+    "tc_comm_set_tuning": (_c_int, [_vp, _c_int, _c_int, _c_int64]),
+    "tc_comm_set_timeout": (_c_int, [_vp, _c_int64]),
+    "tc_comm_set_debug_absent_rank": (_c_int, [_vp, _c_int]),
+    "tc_comm_async_error": (_c_int, [_vp]),
+    "tc_comm_rank": (_c_int, [_vp]),
+    "tc_comm_nranks": (_c_int, [_vp]),
+    "tc_comm_destroy": (_c_int, [_vp]),
+    "tc_comm_last_launch": (_c_int, [_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int),
+                                     ctypes.POINTER(_c_int)]),
+    "tc_group_create": (_c_int, [_vp, _c_int, _pp, ctypes.POINTER(_c_int64), _pp]),
+    "tc_group_destroy": (_c_int, [_vp]),
+    "tc_allreduce": (_c_int, [_vp, _c_float, _vp]),
+    "tc_sgd_step": (_c_int, [_vp, _vp, _vp, _c_float, _c_float, _c_float, _c_float, _vp]),
+    "tc_easgd_update": (_c_int, [_vp, _vp, _c_float, _vp]),
+}
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"libtc.so not built at {path}: run `python build_libtc.py`"
+                          " (there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = load()
+
+
+class TcError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{what}: {STATUS.get(status, status)}")
+
+
+def _check(st: int, what: str):
+    if st != TC_OK:
+        raise TcError(st, what)
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def make_allgather(pg=None):
+    """A tc_allgather_fn over a torch.distributed (gloo/CPU) group."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(pg)
+
+    def cb(ctx, send, recv, nbytes):
+        try:
+            buf = torch.empty(nbytes, dtype=torch.uint8)
+            ctypes.memmove(buf.data_ptr(), send, nbytes)
+            outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(outs, buf, group=pg)
+            for r, o in enumerate(outs):
+                ctypes.memmove(recv + r * nbytes, o.data_ptr(), nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to C as TC_ERR_BOOTSTRAP
+            return 1
+
+    return ALLGATHER_FN(cb)
+
+
+class Plan:
+    """A1 descriptor (host only).  Collective over `pg` when given."""
+
+    def __init__(self, numels: Sequence[int], nranks: int = 1, rank: int = 0, pg=None):
+        arr = (ctypes.c_int64 * len(numels))(*[int(n) for n in numels])
+        self._ag = make_allgather(pg) if pg is not None else ALLGATHER_FN()
+        h = ctypes.c_void_p()
+        _check(LIB.tc_plan_create(rank, nranks, len(numels), arr, self._ag, None, ctypes.byref(h)),
+               "tc_plan_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            LIB.tc_plan_destroy(self.h)
+            self.h = None
+
+    @property
+    def num_elements(self) -> int:
+        return LIB.tc_plan_num_elements(self.h)
+
+    @property
+    def num_slots(self) -> int:
+        return LIB.tc_plan_num_slots(self.h)
+
+    @property
+    def hash(self) -> int:
+        return LIB.tc_plan_hash(self.h)
+
+    def tensor_slots(self, t: int):
+        a, n = ctypes.c_int64(), ctypes.c_int64()
+        _check(LIB.tc_plan_tensor_slots(self.h, t, ctypes.byref(a), ctypes.byref(n)), "tensor_slots")
+        return a.value, n.value
+
+    def owner_range(self, r: int):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(LIB.tc_plan_owner_range(self.h, r, ctypes.byref(a), ctypes.byref(b)), "owner_range")
+        return a.value, b.value
+
+    def segments(self):
+        out = []
+        for i in range(LIB.tc_plan_num_segments(self.h)):
+            t, o, lo, hi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+            _check(LIB.tc_plan_segment(self.h, i, ctypes.byref(t), ctypes.byref(o),
+                                       ctypes.byref(lo), ctypes.byref(hi)), "segment")
+            out.append((t.value, o.value, lo.value, hi.value))
+        return out
+
+
+class Comm:
+    """A tc_comm.  Use :meth:`from_process_group` (one rank per process) or :meth:`emulated`."""
+
+    def __init__(self, handle, ag=None, pg=None):
+        self.h = handle
+        self._ag = ag      # keeps the ctypes callback alive
+        self._pg = pg
+        self.groups = 0
+
+    @classmethod
+    def from_process_group(cls, pg=None, device: int | None = None):
+        """Collective over the ranks of `pg` (default: the world).  Bootstraps over a gloo group
+        with the same ranks (the data path never touches it)."""
+        import torch
+        import torch.distributed as dist
+
+        if device is None:
+            device = torch.cuda.current_device()
+        ranks = None if pg is None else dist.get_process_group_ranks(pg)
+        boot = dist.new_group(ranks=ranks, backend="gloo")
+        ag = make_allgather(boot)
+        h = ctypes.c_void_p()
+        _check(LIB.tc_comm_create(dist.get_rank(boot), dist.get_world_size(boot), device, ag, None,
+                                  ctypes.byref(h)), "tc_comm_create")
+        return cls(h, ag, boot)
+
+    @classmethod
+    def single(cls, device: int = 0):
+        h = ctypes.c_void_p()
+        _check(LIB.tc_comm_create(0, 1, device, ALLGATHER_FN(), None, ctypes.byref(h)),
+               "tc_comm_create")
+        return cls(h)
+
+    @classmethod
+    def emulated(cls, nranks: int, device: int = 0):
+        h = ctypes.c_void_p()
+        _check(LIB.tc_comm_create_emulated(nranks, device, ctypes.byref(h)),
+               "tc_comm_create_emulated")
+        return cls(h)
+
+    @property
+    def rank(self) -> int:
+        return LIB.tc_comm_rank(self.h)
+
+    @property
+    def nranks(self) -> int:
+        return LIB.tc_comm_nranks(self.h)
+
+    @property
+    def is_emulated(self) -> bool:
+        return self.rank < 0
+
+    def set_tuning(self, num_ctas: int = 0, threads: int = 0, oneshot_max_bytes: int = -1):
+        _check(LIB.tc_comm_set_tuning(self.h, num_ctas, threads, oneshot_max_bytes), "set_tuning")
+
+    def set_timeout(self, ms: int):
+        _check(LIB.tc_comm_set_timeout(self.h, int(ms)), "set_timeout")
+
+    def set_debug_absent_rank(self, r: int):
+        _check(LIB.tc_comm_set_debug_absent_rank(self.h, r), "set_debug_absent_rank")
+
+    def async_error(self) -> int:
+        return LIB.tc_comm_async_error(self.h)
+
+    def last_launch(self):
+        a, c, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(LIB.tc_comm_last_launch(self.h, ctypes.byref(a), ctypes.byref(c), ctypes.byref(t)),
+               "last_launch")
+        return ALGO_NAMES.get(a.value, "none"), c.value, t.value
+
+    def destroy(self):
+        if self.h:
+            st = LIB.tc_comm_destroy(self.h)
+            self.h = None
+            _check(st, "tc_comm_destroy")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+
+def _check_tensor(t):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda \
+            or not t.is_contiguous():
+        raise TypeError("tc tensors must be contiguous float32 CUDA tensors")
+
+
+class Group:
+    """A tc_group over `tensors` (this rank's list; for an emulated comm a list per rank)."""
+
+    def __init__(self, comm: Comm, tensors):
+        self.comm = comm
+        if comm.is_emulated:
+            per_rank = [list(ts) for ts in tensors]
+            if len(per_rank) != comm.nranks:
+                raise ValueError("emulated comm: need one tensor list per rank")
+            T = len(per_rank[0])
+            if any(len(ts) != T for ts in per_rank):
+                raise ValueError("emulated comm: ranks disagree on the number of tensors")
+            flat = [t for ts in per_rank for t in ts]
+            numels = [t.numel() for t in per_rank[0]]
+            if any([t.numel() for t in ts] != numels for ts in per_rank):
+                raise TcError(TC_ERR_SHAPE_MISMATCH, "tc_group_create")
+        else:
+            flat = list(tensors)
+            T = len(flat)
+            numels = [t.numel() for t in flat]
+        for t in flat:
+            _check_tensor(t)
+        self.tensors = flat  # keeps the memory alive while the group exists
+        self.numels = numels
+        ptrs = (ctypes.c_void_p * len(flat))(*[t.data_ptr() if t.numel() else None for t in flat])
+        arr = (ctypes.c_int64 * T)(*numels)
+        h = ctypes.c_void_p()
+        _check(LIB.tc_group_create(comm.h, T, ptrs, arr, ctypes.byref(h)), "tc_group_create")
+        self.h = h
+        comm.groups += 1
+
+    def destroy(self):
+        if self.h:
+            st = LIB.tc_group_destroy(self.h)
+            self.h = None
+            self.comm.groups -= 1
+            _check(st, "tc_group_destroy")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+
+def allreduce(x: Group, scale: float = 1.0, stream=None):
+    _check(LIB.tc_allreduce(x.h, float(scale), _stream_ptr(stream)), "tc_allreduce")
+
+
+def sgd_step(w: Group, g: Group, dw: Group, lr: float, momentum: float = 0.0, wd: float = 0.0,
+             rescale: float = 1.0, stream=None):
+    _check(LIB.tc_sgd_step(w.h, g.h, dw.h, float(lr), float(momentum), float(wd), float(rescale),
+                           _stream_ptr(stream)), "tc_sgd_step")
+
+
+def easgd_update(x: Group, center: Group, alpha: float, stream=None):
+    _check(LIB.tc_easgd_update(x.h, center.h, float(alpha), _stream_ptr(stream)),
+           "tc_easgd_update")

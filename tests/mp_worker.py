@@ -1,0 +1,97 @@
+"""Multi-process parity worker: one rank per GPU, launched by torchrun (test_gpu_multiproc.py).
+
+Every rank regenerates every rank's seeded inputs, so each rank checks its own outputs against
+the CPU oracle independently; a failure raises (non-zero exit code).
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import paper_1801_03855_b200 as tc  # noqa: E402
+import tc_workloads as W  # noqa: E402
+from oracle import tc_oracle as O  # noqa: E402
+from gpu_util import to_dev, to_host, assert_bitwise  # noqa: E402
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, p = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    comm = tc.Comm.from_process_group(device=local)
+    assert comm.rank == rank and comm.nranks == p
+
+    # allreduce: tiny config (integer), both algorithms; ragged grad-valued groups
+    cases = [(W.TINY, "int", 0), (W.TINY, "int", 1 << 20),
+             ([7, 13, 1000, 0, 50001, 3, 262144], "grad", 0),
+             ([7, 13, 1000, 0, 5001, 3], "grad", 1 << 20)]
+    for numels, kind, oneshot in cases:
+        comm.set_tuning(0, 0, oneshot)
+        xs = [W.group(numels, kind, 60, 0, k, W.GRAD) for k in range(p)]
+        dev = to_dev(xs[rank])
+        with tc.Group(comm, dev) as g:
+            tc.allreduce(g)
+            assert_bitwise(to_host(dev), O.allreduce(xs), f"allreduce {numels[:4]} rank {rank}")
+        assert comm.async_error() == 0
+
+    # SGD (fused) and EASGD, two-shot and one-shot
+    for oneshot in (0, 1 << 20):
+        comm.set_tuning(0, 0, oneshot)
+        numels = [7, 13, 1000, 4096, 65]
+        gs = [W.group(numels, "grad", 61, 0, k, W.GRAD) for k in range(p)]
+        w = W.group(numels, "param", 61, 0, 0, W.PARAM)
+        dw = W.group(numels, "dw", 61, 0, 0, W.DW)
+        dg, dwt, ddw = to_dev(gs[rank]), to_dev(w), to_dev(dw)
+        hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
+        with tc.Group(comm, dg) as G, tc.Group(comm, dwt) as Wg, tc.Group(comm, ddw) as D:
+            tc.sgd_step(Wg, G, D, **hp)
+            Gw, Ws, Dws = O.sgd_step([w] * p, gs, [dw] * p, **hp)
+            assert_bitwise(to_host(dg), Gw, "sgd g")
+            assert_bitwise(to_host(dwt), Ws[rank], "sgd w")
+            assert_bitwise(to_host(ddw), Dws[rank], "sgd dw")
+        center = W.group(numels, "center", 62, 0, 0, W.CENTER)
+        xs = [W.client_params(numels, center, 62, 0, i) for i in range(p)]
+        dx, dc = to_dev(xs[rank]), to_dev(center)
+        with tc.Group(comm, dx) as X, tc.Group(comm, dc) as C:
+            tc.easgd_update(X, C, 0.1)
+            wx, wc = O.easgd_update(xs, center, 0.1)
+            assert_bitwise(to_host(dx), wx[rank], "easgd x")
+            assert_bitwise(to_host(dc), wc, "easgd center")
+        assert comm.async_error() == 0
+
+    # full-size ResNet-50 gradient group, fused SGD, checked on a sample of elements
+    comm.set_tuning(0, 0, -1)
+    numels = W.RESNET50
+    gs = [W.group(numels, "grad", W.CFG_RESNET50, 0, k, W.GRAD) for k in range(p)]
+    w = W.group(numels, "param", W.CFG_RESNET50, 0, 0, W.PARAM)
+    dw = W.group(numels, "dw", W.CFG_RESNET50, 0, 0, W.DW)
+    dg, dwt, ddw = to_dev(gs[rank]), to_dev(w), to_dev(dw)
+    hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
+    with tc.Group(comm, dg) as G, tc.Group(comm, dwt) as Wg, tc.Group(comm, ddw) as D:
+        tc.sgd_step(Wg, G, D, **hp)
+        hg, hw, hd = to_host(dg), to_host(dwt), to_host(ddw)
+    rng = np.random.default_rng(rank)
+    for t in list(range(0, len(numels), 7)) + [len(numels) - 1]:
+        idx = rng.integers(0, numels[t], size=min(64, numels[t]))
+        sub = lambda grp: [grp[t][idx]]  # noqa: E731
+        Gw, Ws, Dws = O.sgd_step([sub(w)] * p, [sub(g) for g in gs], [sub(dw)] * p, **hp)
+        assert_bitwise([hg[t][idx]], Gw, f"resnet g t={t}")
+        assert_bitwise([hw[t][idx]], Ws[0], f"resnet w t={t}")
+        assert_bitwise([hd[t][idx]], Dws[0], f"resnet dw t={t}")
+    assert comm.async_error() == 0
+    comm.destroy()
+    dist.barrier()
+    if rank == 0:
+        print(f"MP_WORKER_OK p={p}", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

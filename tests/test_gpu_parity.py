@@ -1,0 +1,302 @@
+"""T2: GPU parity of libtc against the CPU oracle, on one B200.
+
+Multi-rank paths run on one GPU through an *emulated* comm: one cooperative kernel whose
+blockIdx.y is the rank, executing the same per-rank code and flag protocol as the
+one-process-per-GPU layout (test_gpu_multiproc.py covers real multi-GPU runs).
+
+Bar: allreduce bit-exact vs the float64-accumulating oracle for every finite
+input (same canonical order, one rounding); SGD and EASGD bit-exact vs the oracle's fp32
+mirror; every rank bit-identical; and, as the BASELINE bound, within 1e-5 * sum|x| of the
+float64 reference.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1801_03855_b200 as tc  # noqa: E402
+import tc_workloads as W  # noqa: E402
+from oracle import tc_oracle as O  # noqa: E402
+from gpu_util import to_dev, to_host, assert_bitwise  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+ONESHOT = 1 << 20   # force one-shot
+TWOSHOT = 0         # force two-shot
+ALGOS = [("two-shot", TWOSHOT), ("one-shot", ONESHOT)]
+
+
+def _comm(p, oneshot=-1, ctas=0):
+    c = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
+    c.set_tuning(ctas, 0, oneshot)
+    return c
+
+
+def run_allreduce(xs, scale=1.0, oneshot=-1, offset=0, ctas=0):
+    p = len(xs)
+    comm = _comm(p, oneshot, ctas)
+    dev = [to_dev(x, offset=offset) for x in xs]
+    grp = tc.Group(comm, dev if p > 1 else dev[0])
+    tc.allreduce(grp, scale)
+    out = [to_host(d) for d in dev]
+    algo = comm.last_launch()[0]
+    assert comm.async_error() == 0
+    grp.destroy()
+    comm.destroy()
+    return out, algo
+
+
+# ------------------------------------------------------------------ allreduce
+@pytest.mark.parametrize("name,oneshot", ALGOS)
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_tiny_config_allreduce_int(p, name, oneshot):
+    """Config 1 (tiny: 3 tensors of 7, 13, 1000 elems, integer-valued) at p ranks."""
+    xs = [W.group(W.TINY, "int", W.CFG_TINY, 0, k, W.GRAD) for k in range(p)]
+    out, algo = run_allreduce(xs, oneshot=oneshot)
+    assert algo == name
+    want = O.allreduce(xs)
+    for r in range(p):
+        assert_bitwise(out[r], want, f"rank {r}")
+
+
+@pytest.mark.parametrize("name,oneshot", ALGOS)
+@pytest.mark.parametrize("p", [2, 4, 5, 8])
+def test_random_groups_grad_values(p, name, oneshot):
+    """Ragged groups (zero-length, 1-element, tails of 1..3) with gradient-like values:
+    bit-exact vs the float64 oracle and within the BASELINE tolerance of the f64 reference."""
+    g = np.random.default_rng(1000 + p)
+    numels = W.random_numels(g, 37, 3000) + [1, 2, 3, 0, 5]
+    xs = [W.group(numels, "grad", 77, 0, k, W.GRAD) for k in range(p)]
+    out, algo = run_allreduce(xs, oneshot=oneshot, scale=0.125)
+    assert algo == name
+    want = O.allreduce(xs, 0.125)
+    ref = O.allreduce_f64(xs, 0.125)
+    for r in range(p):
+        assert_bitwise(out[r], want, f"rank {r}")
+    for t in range(len(numels)):
+        bound = 1e-5 * 0.125 * sum(np.abs(xs[k][t].astype(np.float64)) for k in range(p))
+        assert (np.abs(out[0][t] - ref[t]) <= bound).all()
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_unaligned_tensors_scalar_path(p):
+    """Tensors starting 4 bytes into their allocation (not 16-B aligned): scalar path."""
+    numels = [7, 13, 1000, 4096, 3]
+    xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
+    for oneshot in (TWOSHOT, ONESHOT):
+        out, _ = run_allreduce(xs, oneshot=oneshot, offset=1)
+        for r in range(p):
+            assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
+
+
+@pytest.mark.parametrize("p", [4, 8])
+def test_fewer_slots_than_ranks(p):
+    """N < p: some owners have empty chunks."""
+    numels = [1, 2] if p == 4 else [3, 0, 1]
+    xs = [W.group(numels, "int", 75, 0, k, W.GRAD) for k in range(p)]
+    out, _ = run_allreduce(xs, oneshot=TWOSHOT)
+    for r in range(p):
+        assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
+
+
+def test_many_tensors_1024():
+    p = 4
+    g = np.random.default_rng(5)
+    numels = W.random_numels(g, 1024, 700)
+    xs = [W.group(numels, "grad", 74, 0, k, W.GRAD) for k in range(p)]
+    for oneshot in (TWOSHOT, ONESHOT):
+        out, _ = run_allreduce(xs, oneshot=oneshot)
+        for r in range(p):
+            assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
+
+
+@pytest.mark.parametrize("ctas", [1, 3, 17])
+def test_cta_counts(ctas):
+    """Sub-range partition across CTAs, including few CTAs (many slots per CTA)."""
+    p = 3
+    numels = [7, 13, 1000, 50000, 9]
+    xs = [W.group(numels, "grad", 73, 0, k, W.GRAD) for k in range(p)]
+    out, _ = run_allreduce(xs, oneshot=TWOSHOT, ctas=ctas)
+    for r in range(p):
+        assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
+
+
+def test_single_rank_scale():
+    xs = [W.group([7, 13, 1000, 4097], "grad", 72, 0, 0, W.GRAD)]
+    out, algo = run_allreduce(xs, scale=0.37)
+    assert algo == "local"
+    assert_bitwise(out[0], O.allreduce(xs, 0.37))
+
+
+def test_repeated_calls_epochs():
+    """Many consecutive calls alternating one-/two-shot on one comm (epoch and staging-parity
+    bookkeeping): x_{n+1} = sum_k x_n = p * x_n exactly for integer data (scale 1/p)."""
+    p = 4
+    comm = tc.Comm.emulated(p, 0)
+    numels = [7, 13, 1000]
+    xs = [W.group(numels, "int", 71, 0, k, W.GRAD) for k in range(p)]
+    dev = [to_dev(x) for x in xs]
+    grp = tc.Group(comm, dev)
+    want = O.allreduce(xs, 1.0 / p)
+    for i in range(40):
+        comm.set_tuning(0, 0, ONESHOT if i % 3 else TWOSHOT)
+        tc.allreduce(grp, 1.0 / p if i == 0 else 1.0 / p)
+        if i == 0:
+            first = [to_host(d) for d in dev]
+    out = [to_host(d) for d in dev]
+    for r in range(p):
+        assert_bitwise(first[r], want, "first call")
+        # afterwards every rank holds the mean; averaging identical values is the identity
+        assert_bitwise(out[r], want, "after 40 calls")
+    assert comm.async_error() == 0
+    grp.destroy()
+    comm.destroy()
+
+
+# ------------------------------------------------------------------ SGD (A6)
+SGD_PERF = dict(lr=0.1, momentum=0.9, wd=1e-4)
+SGD_DYADIC = dict(lr=0.5, momentum=0.5, wd=0.0)
+
+
+def run_sgd(p, numels, kind, hp, oneshot=-1, cfg=W.CFG_RESNET50):
+    rescale = 1.0 / (p * 128)
+    gs = [W.group(numels, kind, cfg, 0, k, W.GRAD) for k in range(p)]
+    w = W.group(numels, "int" if kind == "int" else "param", cfg, 0, 0, W.PARAM)
+    dw = W.group(numels, "int" if kind == "int" else "dw", cfg, 0, 0, W.DW)
+    comm = _comm(p, oneshot)
+    dg = [to_dev(g) for g in gs]
+    dwt = [to_dev(w) for _ in range(p)]
+    ddw = [to_dev(dw) for _ in range(p)]
+    pick = (lambda x: x) if p > 1 else (lambda x: x[0])
+    G, Wg, Dg = (tc.Group(comm, pick(x)) for x in (dg, dwt, ddw))
+    tc.sgd_step(Wg, G, Dg, rescale=rescale, **hp)
+    res = [(to_host(dg[r]), to_host(dwt[r]), to_host(ddw[r])) for r in range(p)]
+    algo = comm.last_launch()[0]
+    assert comm.async_error() == 0
+    for grp in (G, Wg, Dg):
+        grp.destroy()
+    comm.destroy()
+    want = O.sgd_step([w] * p, gs, [dw] * p, rescale=rescale, **hp)
+    return res, want, algo, (gs, w, dw, rescale)
+
+
+@pytest.mark.parametrize("name,oneshot", ALGOS + [("local", -1)])
+@pytest.mark.parametrize("hp", [SGD_PERF, SGD_DYADIC], ids=["perf", "dyadic"])
+def test_sgd_step(name, oneshot, hp):
+    p = 1 if name == "local" else 4
+    numels = [7, 13, 1000, 4096, 1, 0, 65]
+    res, (G, Ws, Dws), algo, _ = run_sgd(p, numels, "grad" if hp is SGD_PERF else "int", hp,
+                                         oneshot)
+    assert algo == name
+    for r in range(p):
+        assert_bitwise(res[r][0], G, f"g rank {r}")
+        assert_bitwise(res[r][1], Ws[r], f"w rank {r}")
+        assert_bitwise(res[r][2], Dws[r], f"dw rank {r}")
+
+
+def test_sgd_tolerance_vs_f64():
+    p = 8
+    numels = [5000, 3, 77]
+    res, _, _, (gs, w, dw, rescale) = run_sgd(p, numels, "grad", SGD_PERF, TWOSHOT)
+    _, wr, dwr = O.sgd_step_f64([w] * p, gs, [dw] * p, rescale=rescale, **SGD_PERF)
+    for t in range(len(numels)):
+        sabs = sum(np.abs(gs[k][t].astype(np.float64)) for k in range(p))
+        bd = 1e-5 * (0.9 * np.abs(dw[t]) + 0.1 * (rescale * sabs + 1e-4 * np.abs(w[t])))
+        assert (np.abs(res[0][2][t] - dwr[0][t]) <= bd + 1e-30).all()
+        bw = 1e-5 * (np.abs(w[t]) + np.abs(res[0][2][t]))
+        assert (np.abs(res[0][1][t] - wr[0][t]) <= bw + 1e-30).all()
+
+
+# ------------------------------------------------------------------ EASGD (A7)
+def run_easgd(c, numels, alpha, oneshot=-1, kind="float"):
+    if kind == "int":
+        center = W.group(numels, "int", W.CFG_EASGD, 0, 0, W.CENTER)
+        xs = [W.group(numels, "int", W.CFG_EASGD, 0, i, W.PARAM) for i in range(c)]
+    else:
+        center = W.group(numels, "center", W.CFG_EASGD, 0, 0, W.CENTER)
+        xs = [W.client_params(numels, center, W.CFG_EASGD, 0, i) for i in range(c)]
+    comm = _comm(c, oneshot)
+    dx = [to_dev(x) for x in xs]
+    dc = [to_dev(center) for _ in range(c)]
+    pick = (lambda x: x) if c > 1 else (lambda x: x[0])
+    X, C = tc.Group(comm, pick(dx)), tc.Group(comm, pick(dc))
+    tc.easgd_update(X, C, alpha)
+    res = [(to_host(dx[i]), to_host(dc[i])) for i in range(c)]
+    algo = comm.last_launch()[0]
+    assert comm.async_error() == 0
+    X.destroy()
+    C.destroy()
+    comm.destroy()
+    return res, xs, center, algo
+
+
+@pytest.mark.parametrize("name,oneshot", ALGOS + [("local", -1)])
+@pytest.mark.parametrize("alpha", [0.1, 0.5, 0.0])
+def test_easgd(name, oneshot, alpha):
+    c = 1 if name == "local" else 4
+    numels = [7, 13, 1000, 4096, 0, 2]
+    res, xs, center, algo = run_easgd(c, numels, alpha, oneshot)
+    assert algo == name
+    wx, wc = O.easgd_update(xs, center, alpha)
+    for i in range(c):
+        assert_bitwise(res[i][0], wx[i], f"x client {i}")
+        assert_bitwise(res[i][1], wc, f"center replica {i}")
+
+
+def test_tiny_config_easgd_int_conservation():
+    """Config 1's EASGD step (4 workers = 4 clients, alpha = 0.1) on integer inputs, plus the
+    alpha = 0.5 conservation pin on the GPU result itself."""
+    c = 4
+    res, xs, center, _ = run_easgd(c, W.TINY, 0.1, kind="int")
+    wx, wc = O.easgd_update(xs, center, 0.1)
+    for i in range(c):
+        assert_bitwise(res[i][0], wx[i])
+        assert_bitwise(res[i][1], wc)
+    res, xs, center, _ = run_easgd(c, W.TINY, 0.5, kind="int", oneshot=TWOSHOT)
+    for t in range(3):
+        before = sum(xs[i][t].astype(np.float64) for i in range(c)) + center[t]
+        after = sum(res[i][0][t].astype(np.float64) for i in range(c)) + res[0][1][t]
+        assert (before == after).all()
+
+
+# ------------------------------------------------------------------ errors and faults (T3)
+def test_errors():
+    comm = tc.Comm.emulated(2, 0)
+    a = [to_dev([np.zeros(5, np.float32)]) for _ in range(2)]
+    b = [to_dev([np.zeros(6, np.float32)]) for _ in range(2)]
+    with pytest.raises(tc.TcError) as e:
+        tc.Group(comm, [a[0], b[0]])  # ranks disagree on n_t
+    assert e.value.status == tc.tc.TC_ERR_SHAPE_MISMATCH
+    ga, gb = tc.Group(comm, a), tc.Group(comm, b)
+    with pytest.raises(tc.TcError) as e:
+        tc.easgd_update(ga, gb, 0.1)  # not congruent
+    assert e.value.status == tc.tc.TC_ERR_SHAPE_MISMATCH
+    with pytest.raises(tc.TcError) as e:
+        tc.easgd_update(ga, ga, 1.5)  # alpha outside [0, 1]
+    assert e.value.status == tc.tc.TC_ERR_INVALID_ARG
+    with pytest.raises(tc.TcError) as e:
+        tc.allreduce(ga, float("nan"))
+    assert e.value.status == tc.tc.TC_ERR_INVALID_ARG
+    ga.destroy()
+    gb.destroy()
+    comm.destroy()
+
+
+def test_timeout_when_a_rank_is_absent():
+    """A rank that never arrives: the others time out, the error is sticky, later calls fail."""
+    comm = tc.Comm.emulated(2, 0)
+    comm.set_timeout(200)
+    comm.set_debug_absent_rank(1)
+    xs = [to_dev([np.ones(4096, np.float32)]) for _ in range(2)]
+    grp = tc.Group(comm, xs)
+    comm.set_tuning(0, 0, TWOSHOT)
+    tc.allreduce(grp)
+    torch.cuda.synchronize()
+    assert comm.async_error() == tc.tc.TC_ERR_TIMEOUT
+    with pytest.raises(tc.TcError) as e:
+        tc.allreduce(grp)
+    assert e.value.status == tc.tc.TC_ERR_TIMEOUT
+    grp.destroy()
+    comm.destroy()

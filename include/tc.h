@@ -126,12 +126,24 @@ TC_API tc_status tc_comm_create_emulated(int nranks, int cuda_device, tc_comm** 
  * calls.  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t oneshot_max_bytes);
 
+/* Large-group algorithm (must be identical on all ranks): 0 = automatic, 1 = two-shot with
+ * pulled reduce-scatter (loads from peers' tensors), 3 = two-shot with pushed reduce-scatter
+ * (stores into the owners' receive scratch).  Both end with the staged pull allgather and give
+ * bit-identical results.  Errors: TC_ERR_INVALID_ARG. */
+TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
+
 /* Device-barrier timeout in milliseconds (default 30000, or env TC_TIMEOUT_MS). */
 TC_API tc_status tc_comm_set_timeout(tc_comm* comm, int64_t timeout_ms);
 
 /* Fault injection for tests (emulated comms only): the CTAs of rank `absent_rank` return
  * immediately without arriving at any barrier (-1 = off), so the other ranks time out. */
 TC_API tc_status tc_comm_set_debug_absent_rank(tc_comm* comm, int absent_rank);
+
+/* Diagnostics: when `device_buffer` is non-NULL, hot-path kernels with at most bytes/64 CTAs
+ * (all local ranks) record %globaltimer (ns) at their phase boundaries: slot [cta][0..5] =
+ * start, after entry barrier, after reduce-scatter, after mid barrier, after allgather, end
+ * (CTA index = rank_local * ctas + blockIdx.x).  NULL turns it off.  Not collective. */
+TC_API tc_status tc_comm_set_profile_buffer(tc_comm* comm, void* device_buffer, int64_t bytes);
 
 /* Sticky device-side error: TC_ERR_TIMEOUT once any barrier timed out, else TC_OK.  Reads
  * host-mapped memory; does not synchronize.  After a timeout the comm must be destroyed. */
@@ -197,7 +209,8 @@ TC_API tc_status tc_sgd_step(tc_group* w, tc_group* g, tc_group* dw, float lr, f
 TC_API tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream);
 
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
- * algorithm (0 = local p=1, 1 = two-shot, 2 = one-shot), grid CTAs per rank, threads. */
+ * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push), grid CTAs per
+ * rank, threads. */
 TC_API tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads);
 
 #ifdef __cplusplus

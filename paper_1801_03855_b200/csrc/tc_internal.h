@@ -25,7 +25,7 @@ constexpr int64_t kDefaultOneshotMax = 256 << 10;
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
-enum Algo { ALGO_LOCAL = 0, ALGO_TWOSHOT = 1, ALGO_ONESHOT = 2 };
+enum Algo { ALGO_LOCAL = 0, ALGO_TWOSHOT = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT_PUSH = 3 };
 
 // ---------------------------------------------------------------- A1 descriptor (host)
 struct Plan {
@@ -63,18 +63,22 @@ struct KParams {
   float* const* c;       // [p*T] dw (sgd)
   uint32_t* const* flags;// [p] flag buffers (peer-mapped)
   float* const* stage;   // [p] one-shot staging buffers (peer-mapped), parity-selected
+  float* const* arena;   // [p] per-rank arena: staging chunk x2 (parity) + p receive scratch
+  int chunk_cap;         // slots per arena region (>= the largest owner chunk)
   uint32_t epoch;
   int stage_off;         // float offset of this call's parity half
   float scale, lr, mu, wd, rescale, alpha;
   unsigned long long timeout_ns;
   int* err;              // host-mapped sticky error word
   int absent_rank;       // fault injection (emulated only), -1 off
+  unsigned long long* prof; // optional per-CTA phase timestamps [nlocal*ctas][8] (ns)
 };
 
 // Kernel launchers (tc_kernels.cu).
+// `variant` selects an alternative launch shape for experiments (env TC_VARIANT; 0 = default).
 cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int threads, int nlocal,
-                       bool cooperative, cudaStream_t stream);
-int max_ctas_per_sm(int op, int algo, int p, int threads);
+                       bool cooperative, cudaStream_t stream, int variant);
+int max_ctas_per_sm(int op, int algo, int p, int threads, int variant);
 
 // ---------------------------------------------------------------- runtime objects
 struct MappedBase {
@@ -98,10 +102,18 @@ struct Comm {
   int* h_err = nullptr;           // host-mapped
   int* d_err = nullptr;
   uint32_t epoch = 0;
+  std::array<float*, kMaxRanks> arena{};
+  float** d_arena = nullptr;      // device table [p]
+  int64_t arena_cap = 0;          // slots per region
+  std::vector<std::pair<int, std::string>> arena_keys;  // peer arena mappings held
+  int algo_override = 0;          // 0 auto, else an Algo
+  int variant = 0;                // launch-shape experiment (env TC_VARIANT)
   int tune_ctas = 0, tune_threads = 512;
   int64_t tune_oneshot = -1;
   unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;
   int absent_rank = -1;
+  unsigned long long* prof = nullptr;
+  int64_t prof_slots = 0;
   int last_algo = -1, last_ctas = 0, last_threads = 0;
   std::atomic<bool> busy{false};
   int live_groups = 0;

@@ -85,6 +85,7 @@ tc_status finish_comm(Comm& c) {
   TC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
   c.num_sms = sms;
   c.timeout_ns = env_timeout_ns();
+  c.variant = std::getenv("TC_VARIANT") ? std::atoi(std::getenv("TC_VARIANT")) : 0;
   return TC_OK;
 }
 
@@ -166,6 +167,58 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
 
 bool finite(float v) { return std::isfinite(v); }
 
+// Grow the per-rank arena (staging chunk x2 + p receive scratch regions of `cap` slots each) to
+// hold owner chunks of `need` slots.  Collective (called from tc_group_create on every rank).
+tc_status grow_arena(Comm& c, int64_t need) {
+  const int p = c.nranks;
+  if (p == 1 || need <= c.arena_cap) return TC_OK;
+  int64_t cap = std::max<int64_t>(need, (int64_t)1 << 16);
+  cap = (cap + 4095) & ~(int64_t)4095;
+  const size_t bytes = (size_t)(2 + p) * (size_t)cap * 16;
+  TC_CUDA(cudaDeviceSynchronize());
+  tc_status st = comm_barrier(c);  // no kernel on any rank still uses the old arenas
+  if (st != TC_OK) return st;
+  for (auto& k : c.arena_keys) unmap_peer(c, k);
+  c.arena_keys.clear();
+  for (int r = 0; r < p; ++r) {
+    if (c.emulated || r == c.rank) cudaFree(c.arena[r]);
+    c.arena[r] = nullptr;
+  }
+  st = TC_OK;
+  const int lo = c.emulated ? 0 : c.rank, hi = c.emulated ? p : c.rank + 1;
+  for (int r = lo; r < hi && st == TC_OK; ++r)
+    if (cudaMalloc((void**)&c.arena[r], bytes) != cudaSuccess) st = TC_ERR_CUDA;
+  if (!c.emulated) {
+    struct H { int32_t status; cudaIpcMemHandle_t h; } mine{}, all[kMaxRanks];
+    mine.status = st;
+    if (st == TC_OK && cudaIpcGetMemHandle(&mine.h, c.arena[c.rank]) != cudaSuccess)
+      mine.status = TC_ERR_CUDA;
+    st = bootstrap_allgather(c.ag, c.ag_ctx, p, &mine, all, sizeof(H));
+    for (int r = 0; r < p && st == TC_OK; ++r)
+      if (all[r].status != TC_OK) st = (tc_status)all[r].status;
+    for (int r = 0; r < p && st == TC_OK; ++r) {
+      if (r == c.rank) continue;
+      void* ptr = nullptr;
+      std::pair<int, std::string> key;
+      st = map_peer(c, r, all[r].h, &ptr, &key);
+      if (st == TC_OK) {
+        c.arena[r] = (float*)ptr;
+        c.arena_keys.push_back(key);
+      }
+    }
+    st = agree(c, st);
+  }
+  if (st == TC_OK) {
+    if (!c.d_arena) TC_CUDA(cudaMalloc((void**)&c.d_arena, sizeof(float*) * kMaxRanks));
+    TC_CUDA(cudaMemcpy(c.d_arena, c.arena.data(), sizeof(float*) * kMaxRanks,
+                       cudaMemcpyHostToDevice));
+    c.arena_cap = cap;
+  } else {
+    c.arena_cap = 0;
+  }
+  return st;
+}
+
 // ------------------------------------------------------------------ hot-path dispatcher
 tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr, float mu,
                   float wd, float rescale, float alpha, cudaStream_t stream) {
@@ -190,6 +243,8 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.c = gc ? gc->d_ptrs : nullptr;
   kp.flags = c.d_flags;
   kp.stage = c.d_stage;
+  kp.arena = c.d_arena;
+  kp.chunk_cap = (int)c.arena_cap;
   kp.scale = scale;
   kp.lr = lr;
   kp.mu = mu;
@@ -211,19 +266,22 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   } else {
     int64_t lim = c.tune_oneshot < 0 ? kDefaultOneshotMax : c.tune_oneshot;
     if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
-    algo = bytes <= lim ? ALGO_ONESHOT : ALGO_TWOSHOT;
+    algo = bytes <= lim ? ALGO_ONESHOT : (c.algo_override == ALGO_TWOSHOT_PUSH ? ALGO_TWOSHOT_PUSH
+                                                                              : ALGO_TWOSHOT);
+    if (algo != ALGO_ONESHOT && (pl.M + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   }
   const int nlocal = c.emulated ? p : 1;
-  int occ = max_ctas_per_sm(op, algo, p, threads);
+  int occ = max_ctas_per_sm(op, algo, p, threads, c.variant);
   if (occ < 1) return TC_ERR_CUDA;
   int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
   if (cap < 1) cap = 1;
-  int64_t work_slots = (algo == ALGO_TWOSHOT) ? (pl.M + p - 1) / p : pl.M;
+  const bool twoshot = algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH;
+  int64_t work_slots = twoshot ? (pl.M + p - 1) / p : pl.M;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
   if (algo == ALGO_LOCAL) {
     ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * occ);
-  } else if (algo == ALGO_TWOSHOT && c.tune_ctas > 0) {
+  } else if (twoshot && c.tune_ctas > 0) {
     ctas = c.tune_ctas;
   } else {
     ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * (algo == ALGO_ONESHOT ? 1 : occ));
@@ -233,9 +291,11 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     if (ctas > cap) ctas = cap;
   }
   if (ctas < 1) ctas = 1;
+  if (c.prof && (int64_t)ctas * nlocal <= c.prof_slots) kp.prof = c.prof;
   kp.epoch = ++c.epoch;
   kp.stage_off = (int)((kp.epoch & 1u) * (kStageCapacity / sizeof(float)));
-  cudaError_t e = launch_hot(op, algo, kp, ctas, threads, nlocal, c.emulated && p > 1, stream);
+  cudaError_t e = launch_hot(op, algo, kp, ctas, threads, nlocal, c.emulated && p > 1, stream,
+                             c.variant);
   if (e != cudaSuccess) {
     if (std::getenv("TC_DEBUG"))
       std::fprintf(stderr, "libtc: launch failed: %s\n", cudaGetErrorString(e));
@@ -370,6 +430,13 @@ tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t o
   return TC_OK;
 }
 
+tc_status tc_comm_set_algorithm(tc_comm* comm, int algo) {
+  if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH))
+    return TC_ERR_INVALID_ARG;
+  comm->c.algo_override = algo;
+  return TC_OK;
+}
+
 tc_status tc_comm_set_timeout(tc_comm* comm, int64_t timeout_ms) {
   if (!comm || timeout_ms <= 0) return TC_ERR_INVALID_ARG;
   comm->c.timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
@@ -380,6 +447,13 @@ tc_status tc_comm_set_debug_absent_rank(tc_comm* comm, int absent_rank) {
   if (!comm || !comm->c.emulated || absent_rank < -1 || absent_rank >= comm->c.nranks)
     return TC_ERR_INVALID_ARG;
   comm->c.absent_rank = absent_rank;
+  return TC_OK;
+}
+
+tc_status tc_comm_set_profile_buffer(tc_comm* comm, void* device_buffer, int64_t bytes) {
+  if (!comm || bytes < 0 || (bytes > 0 && !device_buffer)) return TC_ERR_INVALID_ARG;
+  comm->c.prof = (unsigned long long*)device_buffer;
+  comm->c.prof_slots = bytes / (8 * sizeof(unsigned long long));
   return TC_OK;
 }
 
@@ -412,8 +486,10 @@ tc_status tc_comm_destroy(tc_comm* comm) {
     if (c.emulated || r == c.rank) {
       cudaFree(c.flags[r]);
       cudaFree(c.stage[r]);
+      cudaFree(c.arena[r]);
     }
   }
+  cudaFree(c.d_arena);
   cudaFree(c.d_flags);
   cudaFree(c.d_stage);
   cudaFreeHost(c.h_err);
@@ -563,6 +639,7 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
   }
   st = upload_group(g, vec_ok);
   if (!c.emulated && p > 1) st = agree(c, st);
+  if (st == TC_OK) st = grow_arena(c, (g.plan.M + p - 1) / p + 1);
   if (st != TC_OK) {
     free_group_device(g);
     for (auto& k : g.mapped_keys) unmap_peer(c, k);

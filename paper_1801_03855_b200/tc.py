@@ -27,7 +27,8 @@ STATUS = {
 }
 TC_OK, TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_NOT_SHAREABLE = 0, 1, 2, 3
 TC_ERR_BUSY, TC_ERR_TIMEOUT, TC_ERR_CUDA, TC_ERR_BOOTSTRAP, TC_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
-ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot"}
+ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 3: "two-shot-push"}
+ALGO_AUTO, ALGO_TWOSHOT_PULL, ALGO_TWOSHOT_PUSH = 0, 1, 3
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_size_t)
@@ -54,8 +55,10 @@ _SIGS = {
     "tc_comm_create_emulated": (_c_int, [_c_int, _c_int, _pp]),
     "tc_comm_set_tuning": (_c_int, [_vp, _c_int, _c_int, _c_int64]),
     "tc_comm_set_timeout": (_c_int, [_vp, _c_int64]),
+    "tc_comm_set_algorithm": (_c_int, [_vp, _c_int]),
     "tc_comm_set_debug_absent_rank": (_c_int, [_vp, _c_int]),
     "tc_comm_async_error": (_c_int, [_vp]),
+    "tc_comm_set_profile_buffer": (_c_int, [_vp, _vp, _c_int64]),
     "tc_comm_rank": (_c_int, [_vp]),
     "tc_comm_nranks": (_c_int, [_vp]),
     "tc_comm_destroy": (_c_int, [_vp]),
@@ -183,15 +186,17 @@ class Comm:
 
     @classmethod
     def from_process_group(cls, pg=None, device: int | None = None):
-        """Collective over the ranks of `pg` (default: the world).  Bootstraps over a gloo group
-        with the same ranks (the data path never touches it)."""
+        """Collective over the ranks of `pg`.  The bootstrap allgather runs on CPU tensors, so
+        `pg` must be a gloo group (create sub-communicators with
+        ``dist.new_group(ranks, backend="gloo")`` on every rank).  With pg=None a gloo group over
+        the whole world is created (a collective over all ranks).  The data path never touches
+        the process group."""
         import torch
         import torch.distributed as dist
 
         if device is None:
             device = torch.cuda.current_device()
-        ranks = None if pg is None else dist.get_process_group_ranks(pg)
-        boot = dist.new_group(ranks=ranks, backend="gloo")
+        boot = dist.new_group(backend="gloo") if pg is None else pg
         ag = make_allgather(boot)
         h = ctypes.c_void_p()
         _check(LIB.tc_comm_create(dist.get_rank(boot), dist.get_world_size(boot), device, ag, None,
@@ -227,11 +232,24 @@ class Comm:
     def set_tuning(self, num_ctas: int = 0, threads: int = 0, oneshot_max_bytes: int = -1):
         _check(LIB.tc_comm_set_tuning(self.h, num_ctas, threads, oneshot_max_bytes), "set_tuning")
 
+    def set_algorithm(self, algo: int):
+        """0 = automatic, 1 = two-shot pull, 3 = two-shot push (identical results)."""
+        _check(LIB.tc_comm_set_algorithm(self.h, int(algo)), "set_algorithm")
+
     def set_timeout(self, ms: int):
         _check(LIB.tc_comm_set_timeout(self.h, int(ms)), "set_timeout")
 
     def set_debug_absent_rank(self, r: int):
         _check(LIB.tc_comm_set_debug_absent_rank(self.h, r), "set_debug_absent_rank")
+
+    def set_profile_buffer(self, tensor=None):
+        """Diagnostics: phase timestamps into a CUDA int64 tensor of shape [ctas, 8] (or None)."""
+        if tensor is None:
+            _check(LIB.tc_comm_set_profile_buffer(self.h, None, 0), "set_profile_buffer")
+        else:
+            _check(LIB.tc_comm_set_profile_buffer(self.h, tensor.data_ptr(),
+                                                  tensor.numel() * tensor.element_size()),
+                   "set_profile_buffer")
 
     def async_error(self) -> int:
         return LIB.tc_comm_async_error(self.h)

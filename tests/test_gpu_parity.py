@@ -24,12 +24,16 @@ from gpu_util import to_dev, to_host, assert_bitwise  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 ONESHOT = 1 << 20   # force one-shot
-TWOSHOT = 0         # force two-shot
-ALGOS = [("two-shot", TWOSHOT), ("one-shot", ONESHOT)]
+TWOSHOT = 0         # force two-shot (pull reduce-scatter)
+PUSH = -2           # force two-shot with pushed reduce-scatter
+ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT)]
 
 
 def _comm(p, oneshot=-1, ctas=0):
     c = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
+    if oneshot == PUSH:
+        c.set_algorithm(3)
+        oneshot = 0
     c.set_tuning(ctas, 0, oneshot)
     return c
 
@@ -85,7 +89,7 @@ def test_unaligned_tensors_scalar_path(p):
     """Tensors starting 4 bytes into their allocation (not 16-B aligned): scalar path."""
     numels = [7, 13, 1000, 4096, 3]
     xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, ONESHOT):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT):
         out, _ = run_allreduce(xs, oneshot=oneshot, offset=1)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -96,9 +100,10 @@ def test_fewer_slots_than_ranks(p):
     """N < p: some owners have empty chunks."""
     numels = [1, 2] if p == 4 else [3, 0, 1]
     xs = [W.group(numels, "int", 75, 0, k, W.GRAD) for k in range(p)]
-    out, _ = run_allreduce(xs, oneshot=TWOSHOT)
-    for r in range(p):
-        assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
+    for oneshot in (TWOSHOT, PUSH):
+        out, _ = run_allreduce(xs, oneshot=oneshot)
+        for r in range(p):
+            assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
 
 
 def test_many_tensors_1024():
@@ -106,7 +111,7 @@ def test_many_tensors_1024():
     g = np.random.default_rng(5)
     numels = W.random_numels(g, 1024, 700)
     xs = [W.group(numels, "grad", 74, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, ONESHOT):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -118,9 +123,10 @@ def test_cta_counts(ctas):
     p = 3
     numels = [7, 13, 1000, 50000, 9]
     xs = [W.group(numels, "grad", 73, 0, k, W.GRAD) for k in range(p)]
-    out, _ = run_allreduce(xs, oneshot=TWOSHOT, ctas=ctas)
-    for r in range(p):
-        assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
+    for oneshot in (TWOSHOT, PUSH):
+        out, _ = run_allreduce(xs, oneshot=oneshot, ctas=ctas)
+        for r in range(p):
+            assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
 
 
 def test_single_rank_scale():
@@ -141,7 +147,8 @@ def test_repeated_calls_epochs():
     grp = tc.Group(comm, dev)
     want = O.allreduce(xs, 1.0 / p)
     for i in range(40):
-        comm.set_tuning(0, 0, ONESHOT if i % 3 else TWOSHOT)
+        comm.set_algorithm(3 if i % 2 else 1)
+        comm.set_tuning(0, 0, ONESHOT if i % 3 == 0 else TWOSHOT)
         tc.allreduce(grp, 1.0 / p if i == 0 else 1.0 / p)
         if i == 0:
             first = [to_host(d) for d in dev]
@@ -199,7 +206,7 @@ def test_sgd_step(name, oneshot, hp):
 def test_sgd_tolerance_vs_f64():
     p = 8
     numels = [5000, 3, 77]
-    res, _, _, (gs, w, dw, rescale) = run_sgd(p, numels, "grad", SGD_PERF, TWOSHOT)
+    res, _, _, (gs, w, dw, rescale) = run_sgd(p, numels, "grad", SGD_PERF, PUSH)
     _, wr, dwr = O.sgd_step_f64([w] * p, gs, [dw] * p, rescale=rescale, **SGD_PERF)
     for t in range(len(numels)):
         sabs = sum(np.abs(gs[k][t].astype(np.float64)) for k in range(p))
@@ -254,7 +261,7 @@ def test_tiny_config_easgd_int_conservation():
     for i in range(c):
         assert_bitwise(res[i][0], wx[i])
         assert_bitwise(res[i][1], wc)
-    res, xs, center, _ = run_easgd(c, W.TINY, 0.5, kind="int", oneshot=TWOSHOT)
+    res, xs, center, _ = run_easgd(c, W.TINY, 0.5, kind="int", oneshot=PUSH)
     for t in range(3):
         before = sum(xs[i][t].astype(np.float64) for i in range(c)) + center[t]
         after = sum(res[i][0][t].astype(np.float64) for i in range(c)) + res[0][1][t]
@@ -292,6 +299,7 @@ def test_timeout_when_a_rank_is_absent():
     xs = [to_dev([np.ones(4096, np.float32)]) for _ in range(2)]
     grp = tc.Group(comm, xs)
     comm.set_tuning(0, 0, TWOSHOT)
+    comm.set_algorithm(3)
     tc.allreduce(grp)
     torch.cuda.synchronize()
     assert comm.async_error() == tc.tc.TC_ERR_TIMEOUT

@@ -22,6 +22,8 @@ constexpr int kNumBarriers = 3;                // entry, mid, exit
 constexpr size_t kFlagWords = (size_t)kNumBarriers * kMaxRanks * kMaxCtas;
 constexpr size_t kStageCapacity = 8u << 20;    // one-shot staging bytes per parity
 constexpr int64_t kDefaultOneshotMax = 256 << 10;
+constexpr int kPieceShift = 7;                 // work piece = 128 slots = 2 KiB per operand
+constexpr int kPiece = 1 << kPieceShift;
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
@@ -54,6 +56,7 @@ struct KParams {
   int T;
   int M;                 // total 16-B slots
   const int* prefix;     // [T+1] slot prefix
+  const int* block_t;    // [ceil(M/128)] tensor holding the first slot of each 128-slot block
   const int64_t* numel;  // [T]
   const uint8_t* vec_ok; // [T] primary group 16-B aligned on every rank
   const uint8_t* vec_ok_b; // [T] same for group b (nullptr if unused)
@@ -127,6 +130,7 @@ struct Group {
   std::vector<float*> h_ptrs;    // [p*T] (peer-mapped pointers for real comms)
   float** d_ptrs = nullptr;      // device copy
   int* d_prefix = nullptr;
+  int* d_block_t = nullptr;
   int64_t* d_numel = nullptr;
   uint8_t* d_vec_ok = nullptr;
   std::vector<std::pair<int, std::string>> mapped_keys;  // ipc_cache keys held

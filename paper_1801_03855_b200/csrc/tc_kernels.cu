@@ -3,13 +3,14 @@
 // averaging update (Eqs. elastic1/elastic2).
 //
 // Design:
-//  * One kernel per call.  Each rank runs B CTAs; CTA b of every rank owns the same sub-range b
+//  * One kernel per call.  Each rank runs B CTAs; CTA b of every rank owns the same pieces
 //    of every owner chunk, so cross-GPU synchronisation is per-CTA-pair flag exchange (no grid
 //    sync): the epoch is stored into the peer's flag word [barrier][my rank][b] with
 //    st.release.sys and awaited on the local word with ld.acquire.sys (timeout -> sticky error).
-//  * Inside a CTA, warps take 32*U-slot pieces of the sub-range round-robin and every lane
-//    resolves its slot's tensor (cached binary search over the slot prefix), so a sub-range
-//    holding many tiny tensors (ResNet-50's BN vectors) is spread over all warps.
+//  * Every range is cut into 128-slot pieces dealt round-robin to CTAs, then warps: the GPU
+//    streams one contiguous window at a time (DRAM locality) and ranges holding many tiny
+//    tensors (ResNet-50's BN vectors) are spread over all warps.  Each lane resolves its slot's
+//    tensor from a per-128-slot-block tensor table and caches the tensor's pointers.
 //  * Two-shot, pull (A2-A4): ENTRY barrier -> reduce-scatter: each owned slot pulls the 16-B
 //    vectors of all p ranks over NVLink, sums them in float64 in rank order 0..p-1, rounds once,
 //    applies the epilogue, writes in place and into a parity-selected staging chunk -> MID
@@ -178,65 +179,71 @@ __device__ __forceinline__ void elem(const KParams& kp, int r, const float* in, 
 }
 
 // ------------------------------------------------------------------ slot addressing
-// One lane's slot: flat slot s of tensor t, element offset e, cnt valid elements (1..4).
+// One lane's slot: flat slot s, element offset e inside its tensor, cnt valid elements (1..4).
 struct SlotRef {
-  int s, t, cnt;
+  int s, cnt;
   int64_t e;
   bool vec;  // full 16-B slot and the tensor is 16-B aligned in every group of the call
 };
 
+// Per-lane cache of the current tensor and the NP tensor pointers the phase body needs, so the
+// steady state issues no pointer-table loads (refreshed only when a lane crosses a tensor).
+template <int NP>
 struct TensorCache {
   int t, lo, hi;
   int64_t n;
   bool vec;
+  float* ptr[NP];
 };
 
-__device__ __forceinline__ void resolve(const KParams& kp, TensorCache& c, int s, SlotRef& ref) {
+template <class Body>
+__device__ __forceinline__ void resolve(const KParams& kp, const Body& body,
+                                        TensorCache<Body::NP>& c, int s, SlotRef& ref) {
   if (s < c.lo || s >= c.hi) {
-    // largest t with prefix[t] <= s (then prefix[t+1] > s: empty tensors are skipped)
-    int a = (c.t >= 0 && s >= c.hi) ? c.t + 1 : 0, b = kp.T;
-    while (b - a > 1) {
-      const int m = (a + b) >> 1;
-      if (__ldg(kp.prefix + m) <= s) a = m; else b = m;
-    }
-    c.t = a;
-    c.lo = __ldg(kp.prefix + a);
-    c.hi = __ldg(kp.prefix + a + 1);
-    c.n = __ldg(kp.numel + a);
-    c.vec = __ldg(kp.vec_ok + a) && (!kp.vec_ok_b || __ldg(kp.vec_ok_b + a)) &&
-            (!kp.vec_ok_c || __ldg(kp.vec_ok_c + a));
+    // tensor of the slot's 128-slot block, then forward over tensors ending before s
+    int t = __ldg(kp.block_t + (s >> kPieceShift));
+    while (__ldg(kp.prefix + t + 1) <= s) ++t;
+    c.t = t;
+    c.lo = __ldg(kp.prefix + t);
+    c.hi = __ldg(kp.prefix + t + 1);
+    c.n = __ldg(kp.numel + t);
+    c.vec = __ldg(kp.vec_ok + t) && (!kp.vec_ok_b || __ldg(kp.vec_ok_b + t)) &&
+            (!kp.vec_ok_c || __ldg(kp.vec_ok_c + t));
+    body.bind(t, c.ptr);
   }
   ref.s = s;
-  ref.t = c.t;
   ref.e = (int64_t)(s - c.lo) * 4;
   const int64_t rem = c.n - ref.e;
   ref.cnt = rem >= 4 ? 4 : (int)rem;
   ref.vec = c.vec && ref.cnt == 4;
 }
 
-// Tensor-structured operand: tensor ref.t of `rank` in pointer table `tab` ([p][T]).
-__device__ __forceinline__ float4 ldT(const KParams& kp, float* const* tab, int rank,
-                                      const SlotRef& ref) {
-  const float* base = tab[(size_t)rank * kp.T + ref.t] + ref.e;
-  if (ref.vec) return ld16(base);
-  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  v.x = ld4(base);
-  if (ref.cnt > 1) v.y = ld4(base + 1);
-  if (ref.cnt > 2) v.z = ld4(base + 2);
-  if (ref.cnt > 3) v.w = ld4(base + 3);
-  return v;
-}
-__device__ __forceinline__ void stT(const KParams& kp, float* const* tab, int rank,
-                                    const SlotRef& ref, float4 v) {
-  float* base = tab[(size_t)rank * kp.T + ref.t] + ref.e;
-  if (ref.vec) {
-    st16(base, v);
-    return;
+// Tensor-structured operand at element ref.e of a tensor base pointer.
+template <bool VEC>
+__device__ __forceinline__ float4 ldv(const float* base, const SlotRef& ref) {
+  base += ref.e;
+  if constexpr (VEC) {
+    return ld16(base);
+  } else {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x = ld4(base);
+    if (ref.cnt > 1) v.y = ld4(base + 1);
+    if (ref.cnt > 2) v.z = ld4(base + 2);
+    if (ref.cnt > 3) v.w = ld4(base + 3);
+    return v;
   }
-  st4(base, v.x);
-  if (ref.cnt > 1) st4(base + 1, v.y);
-  if (ref.cnt > 2) st4(base + 2, v.z);
-  if (ref.cnt > 3) st4(base + 3, v.w);
+}
+template <bool VEC>
+__device__ __forceinline__ void stv(float* base, const SlotRef& ref, float4 v) {
+  base += ref.e;
+  if constexpr (VEC) {
+    st16(base, v);
+  } else {
+    st4(base, v.x);
+    if (ref.cnt > 1) st4(base + 1, v.y);
+    if (ref.cnt > 2) st4(base + 2, v.z);
+    if (ref.cnt > 3) st4(base + 3, v.w);
+  }
 }
 
 // Staging / scratch regions of the per-rank arena (flat, slot-indexed relative to a chunk).
@@ -247,27 +254,47 @@ __device__ __forceinline__ float* arena_scratch(const KParams& kp, int rank, int
   return kp.arena[rank] + (size_t)(2 + src) * kp.chunk_cap * 4;
 }
 
-// Warps take 32*U-slot pieces of [lo, hi) round-robin; each lane handles U slots 32 apart.
-// Body: struct with `State`, load(ref, st) (issue every load) and finish(ref, st).
+// [lo, hi) is cut into pieces of kPiece slots dealt round-robin to the CTAs of the grid (then
+// to the warps of a CTA), so at any moment the whole GPU streams one contiguous window of memory
+// (DRAM page locality: +40% over per-CTA contiguous ranges, tools/p2p_probe.cu).  The piece ->
+// CTA map depends only on (lo, hi, gridDim), so CTA b of every rank touches the same pieces of a
+// chunk -- the pairing the per-CTA flags rely on.  A lane handles U slots 32 apart per step.
+// Body: NP cached pointers filled by bind(t, ptr); load<VEC>(ref, ptr, st) issues every load
+// of a slot; finish<VEC>(ref, st) computes and stores.  All U slots' loads precede the first
+// finish.
 template <int U, class Body>
-__device__ __forceinline__ void slot_loop(const KParams& kp, int lo, int hi, Body& body) {
+__device__ __forceinline__ void slot_loop(const KParams& kp, int lo, int hi, const Body& body) {
+  static_assert(kPiece % (32 * U) == 0, "piece must be a multiple of a warp step");
   const int lane_id = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  constexpr int CH = 32 * U;
-  TensorCache tcache{-1, 0, 0, 0, false};
-  for (int base = lo + warp * CH; base < hi; base += nw * CH) {
-    SlotRef ref[U];
+  const int npieces = (hi - lo + kPiece - 1) / kPiece;
+  TensorCache<Body::NP> tc;
+  tc.t = -1;
+  tc.lo = tc.hi = 0;
+  for (int c = blockIdx.x + gridDim.x * warp; c < npieces; c += gridDim.x * nw) {
+    const int pbase = lo + c * kPiece;
+    const int pend = min(hi, pbase + kPiece);
+#pragma unroll 1
+    for (int step = pbase; step < pend; step += 32 * U) {
+      SlotRef ref[U];
+      typename Body::State st[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int s = base + lane_id + 32 * u;
-      if (s < hi) resolve(kp, tcache, s, ref[u]); else ref[u].cnt = 0;
+      for (int u = 0; u < U; ++u) {
+        const int s = step + lane_id + 32 * u;
+        if (s < pend) {
+          resolve(kp, body, tc, s, ref[u]);
+          if (ref[u].vec) body.template load<true>(ref[u], tc.ptr, st[u]);
+          else body.template load<false>(ref[u], tc.ptr, st[u]);
+        } else {
+          ref[u].cnt = 0;
+          ref[u].vec = false;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ref[u].vec) body.template finish<true>(ref[u], st[u]);
+        else if (ref[u].cnt) body.template finish<false>(ref[u], st[u]);
+      }
     }
-    typename Body::State st[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (ref[u].cnt) body.load(ref[u], st[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (ref[u].cnt) body.finish(ref[u], st[u]);
   }
 }
 
@@ -280,9 +307,11 @@ enum SrcKind {
 
 // Reduce P sources, apply the epilogue to this rank's operands; optionally also write the
 // reduced primary value into this rank's staging chunk (for the staged allgather).
+// Cached pointers: [0..2] = this rank's a, b, c tensors, then (SRC_TENSORS) P source tensors.
 template <int OP, int P, int SRC, bool STAGE_OUT>
 struct ReduceBody {
   using N = Needs<OP, PH_RS, P>;
+  static constexpr int NP = 3 + (SRC == SRC_TENSORS ? P : 0);
   const KParams& kp;
   int r;
   int origin;         // first slot of the chunk (flat offsets of staging / scratch)
@@ -290,22 +319,38 @@ struct ReduceBody {
   struct State {
     float4 x[P];
     float4 b, c;
+    float *pa, *pb, *pc;
   };
-  __device__ __forceinline__ void load(const SlotRef& ref, State& st) const {
+  __device__ __forceinline__ void bind(int t, float** ptr) const {
+    const size_t mine = (size_t)r * kp.T + t;
+    ptr[0] = kp.a[mine];
+    ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
+    ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
+    if constexpr (SRC == SRC_TENSORS) {
+#pragma unroll
+      for (int k = 0; k < P; ++k) ptr[3 + (k < P ? k : 0)] = kp.a[(size_t)k * kp.T + t];
+    }
+  }
+  template <bool VEC>
+  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       if constexpr (SRC == SRC_TENSORS) {
-        st.x[k] = ldT(kp, kp.a, k, ref);
+        st.x[k] = ldv<VEC>(ptr[3 + k], ref);
       } else if constexpr (SRC == SRC_SCRATCH) {
-        st.x[k] = (k == r) ? ldT(kp, kp.a, r, ref)
+        st.x[k] = (k == r) ? ldv<VEC>(ptr[0], ref)
                            : ld16(arena_scratch(kp, r, k) + (size_t)(ref.s - origin) * 4);
       } else {
         st.x[k] = ld16(kp.stage[k] + kp.stage_off + (size_t)ref.s * 4);
       }
     }
-    if constexpr (N::loadB) st.b = ldT(kp, kp.b, r, ref);
-    if constexpr (N::loadC) st.c = ldT(kp, kp.c, r, ref);
+    if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
+    if constexpr (N::loadC) st.c = ldv<VEC>(ptr[2], ref);
+    st.pa = ptr[0];
+    st.pb = ptr[1];
+    st.pc = ptr[2];
   }
+  template <bool VEC>
   __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
     float4 oa;
 #pragma unroll
@@ -321,9 +366,9 @@ struct ReduceBody {
       if constexpr (N::storeB) lane(st.b, i) = lb;
       if constexpr (N::storeC) lane(st.c, i) = lc;
     }
-    if constexpr (N::storeA) stT(kp, kp.a, r, ref, oa);
-    if constexpr (N::storeB) stT(kp, kp.b, r, ref, st.b);
-    if constexpr (N::storeC) stT(kp, kp.c, r, ref, st.c);
+    if constexpr (N::storeA) stv<VEC>(st.pa, ref, oa);
+    if constexpr (N::storeB) stv<VEC>(st.pb, ref, st.b);
+    if constexpr (N::storeC) stv<VEC>(st.pc, ref, st.c);
     if constexpr (STAGE_OUT) {
       // EASGD gathers the owner's new center, the other ops the reduced primary value
       st16(stage_out + (size_t)(ref.s - origin) * 4, OP == OP_EASGD ? st.b : oa);
@@ -335,19 +380,32 @@ struct ReduceBody {
 template <int OP>
 struct GatherBody {
   using N = Needs<OP, PH_AG, 2>;
+  static constexpr int NP = 3;
   const KParams& kp;
   int r;
   int origin;
   const float* src;   // owner's staging chunk
   struct State {
     float4 x, a, b, c;
+    float *pa, *pb, *pc;
   };
-  __device__ __forceinline__ void load(const SlotRef& ref, State& st) const {
-    st.x = ld16(src + (size_t)(ref.s - origin) * 4);
-    if constexpr (N::loadA) st.a = ldT(kp, kp.a, r, ref);
-    if constexpr (N::loadB) st.b = ldT(kp, kp.b, r, ref);
-    if constexpr (N::loadC) st.c = ldT(kp, kp.c, r, ref);
+  __device__ __forceinline__ void bind(int t, float** ptr) const {
+    const size_t mine = (size_t)r * kp.T + t;
+    ptr[0] = kp.a[mine];
+    ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
+    ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
   }
+  template <bool VEC>
+  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
+    st.x = ld16(src + (size_t)(ref.s - origin) * 4);
+    if constexpr (N::loadA) st.a = ldv<VEC>(ptr[0], ref);
+    if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
+    if constexpr (N::loadC) st.c = ldv<VEC>(ptr[2], ref);
+    st.pa = ptr[0];
+    st.pb = ptr[1];
+    st.pc = ptr[2];
+  }
+  template <bool VEC>
   __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -360,15 +418,16 @@ struct GatherBody {
       if constexpr (N::storeB) lane(st.b, i) = lb;
       if constexpr (N::storeC) lane(st.c, i) = lc;
     }
-    stT(kp, kp.a, r, ref, st.a);
-    if constexpr (N::storeB) stT(kp, kp.b, r, ref, st.b);
-    if constexpr (N::storeC) stT(kp, kp.c, r, ref, st.c);
+    stv<VEC>(st.pa, ref, st.a);
+    if constexpr (N::storeB) stv<VEC>(st.pb, ref, st.b);
+    if constexpr (N::storeC) stv<VEC>(st.pc, ref, st.c);
   }
 };
 
 // Copy this rank's primary tensors into a flat destination (push to an owner's scratch, or
 // the one-shot staging buffer).
 struct CopyOutBody {
+  static constexpr int NP = 1;
   const KParams& kp;
   int r;
   int origin;
@@ -376,142 +435,137 @@ struct CopyOutBody {
   struct State {
     float4 x;
   };
-  __device__ __forceinline__ void load(const SlotRef& ref, State& st) const {
-    st.x = ldT(kp, kp.a, r, ref);
+  __device__ __forceinline__ void bind(int t, float** ptr) const {
+    ptr[0] = kp.a[(size_t)r * kp.T + t];
   }
+  template <bool VEC>
+  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
+    st.x = ldv<VEC>(ptr[0], ref);
+  }
+  template <bool VEC>
   __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
     st16(dst + (size_t)(ref.s - origin) * 4, st.x);
   }
 };
 
-__device__ __forceinline__ void sub_range(int64_t lo, int64_t hi, int b, int B, int& out_lo,
-                                          int& out_hi) {
-  const int64_t len = hi - lo;
-  out_lo = (int)(lo + len * b / B);
-  out_hi = (int)(lo + len * (b + 1) / B);
-}
-
-__host__ __device__ constexpr int unroll_for(int nsrc) {
-  return nsrc <= 2 ? 4 : (nsrc <= 4 ? 2 : 1);
+// Slots per lane per step: enough independent 16-B loads in flight within the register budget
+// of MINB resident 512-thread CTAs per SM.
+__host__ __device__ constexpr int unroll_for(int nsrc, int minb) {
+  return minb >= 2 ? (nsrc <= 2 ? 2 : 1) : (nsrc <= 2 ? 4 : (nsrc <= 4 ? 2 : 1));
 }
 
 // Staged allgather of every other owner's chunk (rotated start: owner r+1 first).
-template <int OP, int P>
-__device__ __forceinline__ void gather_all(const KParams& kp, int r, int b, int B, int par) {
+template <int OP, int P, int MINB>
+__device__ __forceinline__ void gather_all(const KParams& kp, int r, int par) {
   const int64_t M = kp.M;
 #pragma unroll 1
   for (int j = 1; j < P; ++j) {
     const int q = (r + j) % P;
-    int lo, hi;
-    sub_range(M * q / P, M * (q + 1) / P, b, B, lo, hi);
-    GatherBody<OP> body{kp, r, (int)(M * q / P), arena_stage(kp, q, par)};
-    slot_loop<4>(kp, lo, hi, body);
+    const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
+    GatherBody<OP> body{kp, r, lo, arena_stage(kp, q, par)};
+    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
   }
 }
 
 // ------------------------------------------------------------------ kernels
-template <int OP, int P>
-__global__ void __launch_bounds__(512) k_twoshot_pull(KParams kp) {
+template <int OP, int P, int MINB>
+__global__ void __launch_bounds__(512, MINB) k_twoshot_pull(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
-  const int b = blockIdx.x, B = gridDim.x, par = (int)(kp.epoch & 1u);
+  const int par = (int)(kp.epoch & 1u);
   const int64_t M = kp.M;
   stamp(kp, 0);
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
   stamp(kp, 1);
-  int lo, hi;
-  const int origin = (int)(M * r / P);
-  sub_range(M * r / P, M * (r + 1) / P, b, B, lo, hi);
+  const int lo = (int)(M * r / P), hi = (int)(M * (r + 1) / P);
   {
-    ReduceBody<OP, P, SRC_TENSORS, true> body{kp, r, origin, arena_stage(kp, r, par)};
-    slot_loop<unroll_for(P)>(kp, lo, hi, body);
+    ReduceBody<OP, P, SRC_TENSORS, true> body{kp, r, lo, arena_stage(kp, r, par)};
+    slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
   }
   stamp(kp, 2);
   if (!barrier_all(kp, r, BAR_MID, true)) return;
   stamp(kp, 3);
-  gather_all<OP, P>(kp, r, b, B, par);
+  gather_all<OP, P, MINB>(kp, r, par);
   stamp(kp, 4);
   stamp(kp, 5);
 }
 
-template <int OP, int P>
-__global__ void __launch_bounds__(512) k_twoshot_push(KParams kp) {
+template <int OP, int P, int MINB>
+__global__ void __launch_bounds__(512, MINB) k_twoshot_push(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
-  const int b = blockIdx.x, B = gridDim.x, par = (int)(kp.epoch & 1u);
+  const int par = (int)(kp.epoch & 1u);
   const int64_t M = kp.M;
   stamp(kp, 0);
-  // push my contribution of sub-range b of every other chunk into its owner's scratch
+  // push my contribution to this CTA's pieces of every other chunk into its owner's scratch
 #pragma unroll 1
   for (int j = 1; j < P; ++j) {
     const int q = (r + j) % P;
-    int lo, hi;
-    sub_range(M * q / P, M * (q + 1) / P, b, B, lo, hi);
-    CopyOutBody body{kp, r, (int)(M * q / P), arena_scratch(kp, q, r)};
-    slot_loop<4>(kp, lo, hi, body);
+    const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
+    CopyOutBody body{kp, r, lo, arena_scratch(kp, q, r)};
+    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
     __syncthreads();
     if (threadIdx.x == 0) signal_one(kp, BAR_ENTRY, r, q);
   }
   stamp(kp, 1);
   if (!barrier_all(kp, r, BAR_ENTRY, false)) return;  // every peer's push has landed
-  int lo, hi;
-  const int origin = (int)(M * r / P);
-  sub_range(M * r / P, M * (r + 1) / P, b, B, lo, hi);
+  const int lo = (int)(M * r / P), hi = (int)(M * (r + 1) / P);
   {
-    ReduceBody<OP, P, SRC_SCRATCH, true> body{kp, r, origin, arena_stage(kp, r, par)};
-    slot_loop<unroll_for(P)>(kp, lo, hi, body);
+    ReduceBody<OP, P, SRC_SCRATCH, true> body{kp, r, lo, arena_stage(kp, r, par)};
+    slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
   }
   stamp(kp, 2);
   if (!barrier_all(kp, r, BAR_MID, true)) return;
   stamp(kp, 3);
-  gather_all<OP, P>(kp, r, b, B, par);
+  gather_all<OP, P, MINB>(kp, r, par);
   stamp(kp, 4);
   stamp(kp, 5);
 }
 
-template <int OP, int P>
-__global__ void __launch_bounds__(512) k_oneshot(KParams kp) {
+template <int OP, int P, int MINB>
+__global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
-  int lo, hi;
-  sub_range(0, kp.M, blockIdx.x, gridDim.x, lo, hi);
+  const int lo = 0, hi = kp.M;
   stamp(kp, 0);
   {
     CopyOutBody body{kp, r, 0, kp.stage[r] + kp.stage_off};
-    slot_loop<4>(kp, lo, hi, body);
+    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
   }
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
   stamp(kp, 1);
   ReduceBody<OP, P, SRC_ONESHOT, false> body{kp, r, 0, nullptr};
-  slot_loop<unroll_for(P)>(kp, lo, hi, body);
+  slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
   stamp(kp, 5);
 }
 
 template <int OP, int MINB, int U>
 __global__ void __launch_bounds__(512, MINB) k_local(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
-  int lo, hi;
-  sub_range(0, kp.M, blockIdx.x, gridDim.x, lo, hi);
   ReduceBody<OP, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
-  slot_loop<U>(kp, lo, hi, body);
+  slot_loop<U>(kp, 0, kp.M, body);
 }
 
 template <int OP>
 const void* kernel_ptr(int algo, int p, int variant) {
   if (algo == ALGO_LOCAL) {
     switch (variant) {
-      case 1: return (const void*)k_local<OP, 2, 2>;
+      case 1: return (const void*)k_local<OP, 1, 4>;
       case 2: return (const void*)k_local<OP, 2, 4>;
-      case 3: return (const void*)k_local<OP, 1, 8>;
+      case 3: return (const void*)k_local<OP, 1, 2>;
       case 4: return (const void*)k_local<OP, 3, 2>;
-      default: return (const void*)k_local<OP, 1, 4>;
+      default: return (const void*)k_local<OP, 2, 2>;  // measured best: 2 CTAs/SM, U = 2
     }
   }
-#define TC_CASE(PP)                                                        \
-  case PP:                                                                 \
-    return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP>      \
-         : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP> \
-                                     : (const void*)k_oneshot<OP, PP>;
+#define TC_CASE(PP)                                                                  \
+  case PP:                                                                           \
+    if (variant == 1)                                                                \
+      return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 1>           \
+           : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 1>      \
+                                       : (const void*)k_oneshot<OP, PP, 1>;          \
+    return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 2>             \
+         : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 2>        \
+                                     : (const void*)k_oneshot<OP, PP, 2>;
   switch (p) {
     TC_CASE(2) TC_CASE(3) TC_CASE(4) TC_CASE(5) TC_CASE(6) TC_CASE(7) TC_CASE(8)
     default: return nullptr;

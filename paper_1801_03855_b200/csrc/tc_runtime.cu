@@ -140,10 +140,12 @@ tc_status agree(Comm& c, tc_status mine) {
 void free_group_device(Group& g) {
   cudaFree(g.d_ptrs);
   cudaFree(g.d_prefix);
+  cudaFree(g.d_block_t);
   cudaFree(g.d_numel);
   cudaFree(g.d_vec_ok);
   g.d_ptrs = nullptr;
   g.d_prefix = nullptr;
+  g.d_block_t = nullptr;
   g.d_numel = nullptr;
   g.d_vec_ok = nullptr;
 }
@@ -151,6 +153,16 @@ void free_group_device(Group& g) {
 tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
   const Plan& pl = g.plan;
   std::vector<int> prefix(pl.slot_prefix.begin(), pl.slot_prefix.end());
+  // tensor of the first slot of every 128-slot block (largest t with prefix[t] <= slot)
+  std::vector<int> block_t((size_t)((pl.M + kPiece - 1) >> kPieceShift) + 1, 0);
+  for (size_t j = 0, t = 0; j < block_t.size(); ++j) {
+    const int64_t slot = (int64_t)j << kPieceShift;
+    while (t + 1 < (size_t)pl.T && pl.slot_prefix[t + 1] <= slot) ++t;
+    block_t[j] = (int)t;
+  }
+  TC_CUDA(cudaMalloc((void**)&g.d_block_t, sizeof(int) * block_t.size()));
+  TC_CUDA(cudaMemcpy(g.d_block_t, block_t.data(), sizeof(int) * block_t.size(),
+                     cudaMemcpyHostToDevice));
   TC_CUDA(cudaMalloc((void**)&g.d_ptrs, sizeof(float*) * g.h_ptrs.size()));
   TC_CUDA(cudaMalloc((void**)&g.d_prefix, sizeof(int) * prefix.size()));
   TC_CUDA(cudaMalloc((void**)&g.d_numel, sizeof(int64_t) * pl.numel.size()));
@@ -236,6 +248,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.T = pl.T;
   kp.M = (int)pl.M;
   kp.prefix = ga->d_prefix;
+  kp.block_t = ga->d_block_t;
   kp.numel = ga->d_numel;
   kp.vec_ok = ga->d_vec_ok;
   kp.a = ga->d_ptrs;

@@ -133,6 +133,119 @@ __global__ void __launch_bounds__(32) tma_copy(const char* __restrict__ src, cha
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Local fused-SGD stream on flat buffers (3 reads, 2 writes per element): LDG version.
+__device__ __forceinline__ float4 ldna(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void sgd4(float4 g, float4& w, float4& d) {
+  float* gp = &g.x; float* wp = &w.x; float* dp = &d.x;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float t = __fadd_rn(__fmul_rn(0.01f, gp[i]), __fmul_rn(1e-4f, wp[i]));
+    dp[i] = __fsub_rn(__fmul_rn(0.9f, dp[i]), __fmul_rn(0.1f, t));
+    wp[i] = __fadd_rn(wp[i], dp[i]);
+  }
+}
+template <int U>
+__global__ void sgd_ldg(const float4* __restrict__ g, float4* __restrict__ w, float4* __restrict__ d,
+                        size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x * U + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x * U;
+  for (; i < n; i += stride) {
+    float4 a[U], b[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      size_t j = i + (size_t)u * blockDim.x;
+      if (j < n) { a[u] = ldna(g + j); b[u] = ldna(w + j); c[u] = ldna(d + j); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      size_t j = i + (size_t)u * blockDim.x;
+      if (j < n) { sgd4(a[u], b[u], c[u]); w[j] = b[u]; d[j] = c[u]; }
+    }
+  }
+}
+// Same, but every CTA streams its own contiguous 1/gridDim range (no grid-stride locality).
+template <int U>
+__global__ void sgd_ldg_ranges(const float4* __restrict__ g, float4* __restrict__ w,
+                               float4* __restrict__ d, size_t n) {
+  const size_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+  for (size_t i = lo + threadIdx.x; i < hi; i += (size_t)blockDim.x * U) {
+    float4 a[U], b[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      size_t j = i + (size_t)u * blockDim.x;
+      if (j < hi) { a[u] = ldna(g + j); b[u] = ldna(w + j); c[u] = ldna(d + j); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      size_t j = i + (size_t)u * blockDim.x;
+      if (j < hi) { sgd4(a[u], b[u], c[u]); w[j] = b[u]; d[j] = c[u]; }
+    }
+  }
+}
+// TMA version: warp 0 lane 0 produces (bulk loads of g, w, d tiles into NS stages), the other
+// warps consume from shared memory and store with STG.
+template <int TILE, int NS>
+__global__ void __launch_bounds__(32 * 9) sgd_tma(const float4* __restrict__ g, float4* __restrict__ w,
+                                                  float4* __restrict__ d, size_t n) {
+  extern __shared__ __align__(128) float4 sm4[];
+  __shared__ __align__(8) unsigned long long full[NS], empty[NS];
+  const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  const int ncons = blockDim.x - 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[s])), "r"(ncons));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const size_t ntiles = (n + TILE - 1) / TILE;
+  auto wait = [](unsigned long long* b, uint32_t parity) {
+    asm volatile("{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+                 "@!P bra W_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+  };
+  if (warp == 0) {
+    if (lane_id != 0) return;
+    size_t k = 0;
+    for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+      const int s = (int)(k % NS);
+      if (k >= NS) wait(&empty[s], (uint32_t)(((k / NS) - 1) & 1));
+      const size_t lo = tile * TILE;
+      const uint32_t cnt = (uint32_t)(n - lo < TILE ? n - lo : TILE);
+      const uint32_t bytes = cnt * 16;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(3 * bytes));
+      const float4* src[3] = {g + lo, w + lo, d + lo};
+      for (int o = 0; o < 3; ++o)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_u32(sm4 + ((size_t)s * 3 + o) * TILE)), "l"(src[o]), "r"(bytes),
+                     "r"(smem_u32(&full[s])) : "memory");
+    }
+    return;
+  }
+  size_t k = 0;
+  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = (int)(k % NS);
+    wait(&full[s], (uint32_t)((k / NS) & 1));
+    const size_t lo = tile * TILE;
+    const int cnt = (int)(n - lo < TILE ? n - lo : TILE);
+    const float4* sg = sm4 + ((size_t)s * 3 + 0) * TILE;
+    const float4* sw = sm4 + ((size_t)s * 3 + 1) * TILE;
+    const float4* sd = sm4 + ((size_t)s * 3 + 2) * TILE;
+    for (int i = threadIdx.x - 32; i < cnt; i += ncons) {
+      float4 a = sg[i], b = sw[i], c = sd[i];
+      sgd4(a, b, c);
+      w[lo + i] = b;
+      d[lo + i] = c;
+    }
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+  }
+}
+
 typedef void (*KFn)(const float4*, float4*, size_t);
 
 template <int U, int MODE> KFn kfn() { return copy_kernel<U, MODE>; }
@@ -214,6 +327,39 @@ int main(int argc, char** argv) {
     KFn f = fns[1][2];
     snprintf(name, sizeof name, "local HBM copy %dx512 U=4", grid);
     run(name, [&](int d) { f<<<grid, 512, 0, st[d]>>>(a[d], b[d], nvec); });
+  }
+  {
+    // fused SGD stream (3 reads + 2 writes per element) over 3 flat buffers of bytes/3 each
+    size_t n3 = nvec / 3;
+    double sgd_bytes = 5.0 * n3 * 16;
+    auto runs = [&](const char* nm, auto launch) {
+      for (int rep = 0; rep < 2; ++rep) {
+        for (int d = 0; d < n; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
+        CK(cudaSetDevice(0));
+        CK(cudaEventRecord(e0[0], st[0]));
+        for (int it = 0; it < 5; ++it) launch(0);
+        CK(cudaEventRecord(e1[0], st[0]));
+        CK(cudaEventSynchronize(e1[0]));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0[0], e1[0]));
+        CK(cudaGetLastError());
+        if (rep) printf("%-48s %8.1f GB/s HBM (5 x %zu MB)\n", nm, sgd_bytes * 5 / (ms / 1e3) / 1e9, n3 * 16 >> 20);
+      }
+    };
+    float4* G = a[0]; float4* Wt = a[0] + n3; float4* D = a[0] + 2 * n3;
+    runs("sgd LDG 148x512 U=4", [&](int) { sgd_ldg<4><<<sms, 512, 0, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd LDG 296x512 U=2", [&](int) { sgd_ldg<2><<<2 * sms, 512, 0, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd LDG 296x512 U=4", [&](int) { sgd_ldg<4><<<2 * sms, 512, 0, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd LDG 592x256 U=4", [&](int) { sgd_ldg<4><<<4 * sms, 256, 0, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd LDG ranges 148x512 U=4", [&](int) { sgd_ldg_ranges<4><<<sms, 512, 0, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd LDG ranges 296x512 U=2", [&](int) { sgd_ldg_ranges<2><<<2 * sms, 512, 0, st[0]>>>(G, Wt, D, n3); });
+    CK(cudaFuncSetAttribute(sgd_tma<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * 16 * 3 * 4));
+    CK(cudaFuncSetAttribute(sgd_tma<256, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 16 * 3 * 8));
+    CK(cudaFuncSetAttribute(sgd_tma<1024, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16 * 3 * 4));
+    runs("sgd TMA tile=8K NS=4 148x288", [&](int) { sgd_tma<512, 4><<<sms, 288, 512 * 16 * 3 * 4, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd TMA tile=4K NS=8 148x288", [&](int) { sgd_tma<256, 8><<<sms, 288, 256 * 16 * 3 * 8, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd TMA tile=16K NS=4 148x288", [&](int) { sgd_tma<1024, 4><<<sms, 288, 1024 * 16 * 3 * 4, st[0]>>>(G, Wt, D, n3); });
+    runs("sgd TMA tile=8K NS=4 296x288", [&](int) { sgd_tma<512, 4><<<2 * sms, 288, 512 * 16 * 3 * 4, st[0]>>>(G, Wt, D, n3); });
   }
   run("cudaMemcpyPeerAsync pull", [&](int d) { int q = (d + 1) % n;
     CK(cudaMemcpyPeerAsync(b[d], d, a[q], q, bytes, st[d])); });

@@ -214,7 +214,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--algo", type=int, default=0, help="0 auto, 1 two-shot pull, 3 two-shot push")
+    ap.add_argument("--algo", type=int, default=0,
+                    help="0 auto, 1 two-shot pull, 3 two-shot push, 4 NVLS")
+    ap.add_argument("--no-sym", action="store_true",
+                    help="keep gradients in torch memory (no NVLS) instead of tc_mem_alloc")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -248,6 +251,12 @@ def main():
 
     comm = tc.Comm.single(local) if p == 1 else tc.Comm.from_process_group(device=local)
     comm.set_algorithm(args.algo)
+    sym = p > 1 and not args.no_sym
+    if sym:
+        # the gradient bucket in symmetric multicast memory (tc_mem_alloc): NVLS-eligible
+        g_flat = comm.alloc_symmetric(sum(numels))
+        g_flat.copy_(gp_flat)
+        g = list(torch.split(g_flat, [int(n) for n in numels]))
     G, Wg, D = tc.Group(comm, g), tc.Group(comm, w), tc.Group(comm, dw)
     refresh = p > 1  # at p = 1 the gradient is not modified by the step
 
@@ -416,6 +425,7 @@ def main():
         "config": {"workload": f"{args.config} gradient group: tc_sgd_step (allreduce + fused "
                                f"SGD-momentum), {len(numels)} tensors, {S/1e6:.2f} MB per rank",
                    "global_batch": None, "p": p, "algo": algo, "ctas": ctas, "threads": threads,
+                   "grad_memory": "tc_mem_alloc (symmetric, multicast)" if sym else "torch",
                    "l2": "inputs larger than L2 (3 groups, %.0f MB per GPU); no flush" % (3 * S / 1e6),
                    "parallelism": f"dp{p}"},
         "busbw_gbs": busbw, "algbw_gbs": algbw, "t_us": t_ms * 1e3,

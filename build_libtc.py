@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 HERE = os.path.join(ROOT, "paper_1801_03855_b200")
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtc.so")
-SOURCES = ["tc_plan.cpp", "tc_runtime.cu", "tc_kernels.cu"]
+SOURCES = ["tc_plan.cpp", "tc_runtime.cu", "tc_symmem.cu", "tc_kernels.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

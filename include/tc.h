@@ -128,8 +128,12 @@ TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, in
 
 /* Large-group algorithm (must be identical on all ranks): 0 = automatic, 1 = two-shot with
  * pulled reduce-scatter (loads from peers' tensors), 3 = two-shot with pushed reduce-scatter
- * (stores into the owners' receive scratch).  Both end with the staged pull allgather and give
- * bit-identical results.  Errors: TC_ERR_INVALID_ARG. */
+ * (stores into the owners' receive scratch), 4 = NVLS (switch reduction, multimem.ld_reduce +
+ * multimem.st; only for groups in tc_mem_alloc memory, else two-shot).  1 and 3 end with the
+ * staged pull allgather and give bit-identical results (float64, rank order).  NVLS sums in
+ * the switch in fp32 (order unspecified): exact for integer-valued data, else within
+ * (p-1) ulp-scale of the float64 sum; identical on every rank.  Automatic: p = 2 pull,
+ * p = 3..5 push, p >= 6 NVLS for eligible groups (else push).  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 
 /* Device-barrier timeout in milliseconds (default 30000, or env TC_TIMEOUT_MS). */
@@ -155,6 +159,23 @@ TC_API int tc_comm_nranks(const tc_comm* comm);
 /* Collective: synchronizes the device, waits for every rank (bootstrap barrier), unmaps and
  * frees.  All groups of the comm must have been destroyed first (TC_ERR_INVALID_ARG). */
 TC_API tc_status tc_comm_destroy(tc_comm* comm);
+
+/* ---------------------------------------------------------------------------------------
+ * Symmetric memory (for the NVSwitch multicast algorithm).
+ * --------------------------------------------------------------------------------------- */
+
+/* Collective over a one-rank-per-process comm: allocates `bytes` (rounded up to the
+ * allocation granularity) of device memory on every rank, maps every peer's copy into this
+ * process, and -- when NVSwitch multicast is supported -- binds all copies to one multicast
+ * object.  Returns this rank's pointer.  Tensors placed at the SAME offset of the same
+ * symmetric allocation on every rank can be reduced in the switch (algorithm 4, NVLS:
+ * multimem.ld_reduce / multimem.st).  Freed only by tc_mem_free (collective) or
+ * tc_comm_destroy.  Errors: TC_ERR_INVALID_ARG, TC_ERR_UNSUPPORTED (emulated comm or no VMM
+ * driver entry points), TC_ERR_CUDA, TC_ERR_BOOTSTRAP. */
+TC_API tc_status tc_mem_alloc(tc_comm* comm, size_t bytes, void** ptr);
+TC_API tc_status tc_mem_free(tc_comm* comm, void* ptr);
+/* 1 if this comm's device supports NVSwitch multicast + reduction, else 0. */
+TC_API int tc_comm_multicast_supported(const tc_comm* comm);
 
 /* ---------------------------------------------------------------------------------------
  * Tensor groups (the paper's "tensor", generalized to T tensors per rank).
@@ -209,8 +230,8 @@ TC_API tc_status tc_sgd_step(tc_group* w, tc_group* g, tc_group* dw, float lr, f
 TC_API tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream);
 
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
- * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push), grid CTAs per
- * rank, threads. */
+ * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS), grid
+ * CTAs per rank, threads. */
 TC_API tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads);
 
 #ifdef __cplusplus

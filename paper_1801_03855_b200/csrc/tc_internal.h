@@ -27,7 +27,7 @@ constexpr int kPiece = 1 << kPieceShift;
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
-enum Algo { ALGO_LOCAL = 0, ALGO_TWOSHOT = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT_PUSH = 3 };
+enum Algo { ALGO_LOCAL = 0, ALGO_TWOSHOT = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT_PUSH = 3, ALGO_NVLS = 4 };
 
 // ---------------------------------------------------------------- A1 descriptor (host)
 struct Plan {
@@ -41,6 +41,11 @@ struct Plan {
   int64_t owner_lo(int r) const { return M * r / nranks; }
   int64_t owner_hi(int r) const { return M * (r + 1) / nranks; }
 };
+
+struct Comm;
+int find_sym(const Comm& c, const void* p, size_t bytes, int64_t* offset);
+bool multicast_supported(int device);
+void free_all_sym(Comm& c);
 
 tc_status build_plan(int rank, int nranks, int ntensors, const int64_t* numels, Plan& out);
 uint64_t plan_hash(int ntensors, const int64_t* numels);
@@ -64,6 +69,7 @@ struct KParams {
   float* const* a;       // [p*T] primary group: x (allreduce, easgd) or g (sgd)
   float* const* b;       // [p*T] w (sgd) or center (easgd)
   float* const* c;       // [p*T] dw (sgd)
+  float* const* mc;      // [T] multicast addresses of the primary group (NVLS), or nullptr
   uint32_t* const* flags;// [p] flag buffers (peer-mapped)
   float* const* stage;   // [p] one-shot staging buffers (peer-mapped), parity-selected
   float* const* arena;   // [p] per-rank arena: staging chunk x2 (parity) + p receive scratch
@@ -84,6 +90,18 @@ cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int thread
 int max_ctas_per_sm(int op, int algo, int p, int threads, int variant);
 
 // ---------------------------------------------------------------- runtime objects
+// One symmetric allocation (tc_mem_alloc): every rank's physical memory mapped locally (uc[r]),
+// plus the multicast mapping when NVSwitch multicast is available.
+struct SymAlloc {
+  size_t size = 0;
+  int device = 0;
+  bool multicast = false;
+  uint64_t phys[kMaxRanks] = {};
+  void* uc[kMaxRanks] = {};
+  uint64_t mc_handle = 0;
+  void* mc = nullptr;
+};
+
 struct MappedBase {
   void* ptr = nullptr;
   int refs = 0;
@@ -120,6 +138,7 @@ struct Comm {
   int last_algo = -1, last_ctas = 0, last_threads = 0;
   std::atomic<bool> busy{false};
   int live_groups = 0;
+  std::vector<SymAlloc> sym;      // symmetric allocations, in creation order (same on all ranks)
   // IPC mapping cache: (peer, handle bytes) -> mapping
   std::map<std::pair<int, std::string>, MappedBase> ipc_cache;
 };
@@ -134,6 +153,8 @@ struct Group {
   int64_t* d_numel = nullptr;
   uint8_t* d_vec_ok = nullptr;
   std::vector<std::pair<int, std::string>> mapped_keys;  // ipc_cache keys held
+  std::vector<float*> h_mc;      // [T] multicast addresses (NVLS-eligible groups only)
+  float** d_mc = nullptr;
 };
 
 }  // namespace tc

@@ -109,6 +109,13 @@ __device__ bool barrier_all(const KParams& kp, int r, int bar, bool do_signal) {
   return __syncthreads_and(ok) != 0;
 }
 
+// Whole CTA: publish arrival at `bar` to every peer without waiting.
+__device__ __forceinline__ void signal_all(const KParams& kp, int r, int bar) {
+  __syncthreads();
+  const int k = threadIdx.x;
+  if (k < kp.p && k != r) st_release_sys(kp.flags[k] + flag_index(bar, r, blockIdx.x), kp.epoch);
+}
+
 // ------------------------------------------------------------------ element arithmetic
 enum Phase { PH_RS = 0, PH_AG = 1 };
 
@@ -327,8 +334,9 @@ struct ReduceBody {
     ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
     ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
     if constexpr (SRC == SRC_TENSORS) {
+      // P == 1 (local paths): the single source is this rank's own tensor
 #pragma unroll
-      for (int k = 0; k < P; ++k) ptr[3 + (k < P ? k : 0)] = kp.a[(size_t)k * kp.T + t];
+      for (int k = 0; k < P; ++k) ptr[3 + k] = kp.a[(size_t)(P == 1 ? r : k) * kp.T + t];
     }
   }
   template <bool VEC>
@@ -454,18 +462,117 @@ __host__ __device__ constexpr int unroll_for(int nsrc, int minb) {
   return minb >= 2 ? (nsrc <= 2 ? 2 : 1) : (nsrc <= 2 ? 4 : (nsrc <= 4 ? 2 : 1));
 }
 
-// Staged allgather of every other owner's chunk (rotated start: owner r+1 first).
+// Whole CTA: wait until rank q's CTA has passed `bar`.  Returns false on timeout.
+__device__ bool wait_one(const KParams& kp, int r, int q, int bar) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    const uint32_t* mine = kp.flags[r] + flag_index(bar, q, blockIdx.x);
+    if ((int32_t)(ld_acquire_sys(mine) - kp.epoch) < 0) {
+      const unsigned long long t0 = globaltimer();
+      while ((int32_t)(ld_acquire_sys(mine) - kp.epoch) < 0) {
+        if (globaltimer() - t0 > kp.timeout_ns) {
+          atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  const int ok = s_ok;
+  __syncthreads();
+  return ok != 0;
+}
+
+// Staged allgather: publish my staged chunk, then pull every other owner's chunk once that
+// owner's CTA has staged it.  CTA b visits the owners starting at r+1+(b mod p-1), so at any
+// moment every GPU serves about the same number of readers (a plain rotation by rank would
+// let one slow owner's readers pile up; "whichever is ready first" measured 30% slower at p=4
+// because the early owners' egress saturates).
 template <int OP, int P, int MINB>
-__device__ __forceinline__ void gather_all(const KParams& kp, int r, int par) {
+__device__ __forceinline__ bool gather_all(const KParams& kp, int r, int par) {
   const int64_t M = kp.M;
+  signal_all(kp, r, BAR_MID);
 #pragma unroll 1
-  for (int j = 1; j < P; ++j) {
-    const int q = (r + j) % P;
+  for (int j = 0; j < P - 1; ++j) {
+    const int q = (r + 1 + ((int)blockIdx.x + j) % (P - 1)) % P;
+    if (!wait_one(kp, r, q, BAR_MID)) return false;
     const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
     GatherBody<OP> body{kp, r, lo, arena_stage(kp, q, par)};
     slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
   }
+  return true;
 }
+
+// ------------------------------------------------------------------ NVLS (switch reduction)
+// multimem.ld_reduce on a multicast address returns the sum of every rank's copy, reduced in
+// the NVSwitch (fp32, order chosen by the switch); multimem.st writes every rank's copy.
+__device__ __forceinline__ float4 mm_ld_reduce16(const float* p) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float mm_ld_reduce4(const float* p) {
+  float v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mm_st16(float* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st4(float* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// Owner side of NVLS: reduce every rank's copy of an owned slot in the switch, apply the
+// allreduce scale, multicast-store the result into every rank's copy.
+template <int OP>
+struct NvlsBody {
+  static constexpr int NP = 1;
+  const KParams& kp;
+  int r;
+  struct State {
+    float4 v;
+    float* mp;
+  };
+  __device__ __forceinline__ void bind(int t, float** ptr) const { ptr[0] = kp.mc[t]; }
+  template <bool VEC>
+  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
+    st.mp = ptr[0] + ref.e;
+    if constexpr (VEC) {
+      st.v = mm_ld_reduce16(st.mp);
+    } else {
+      st.v = make_float4(0.f, 0.f, 0.f, 0.f);
+      st.v.x = mm_ld_reduce4(st.mp);
+      if (ref.cnt > 1) st.v.y = mm_ld_reduce4(st.mp + 1);
+      if (ref.cnt > 2) st.v.z = mm_ld_reduce4(st.mp + 2);
+      if (ref.cnt > 3) st.v.w = mm_ld_reduce4(st.mp + 3);
+    }
+  }
+  template <bool VEC>
+  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
+    if constexpr (OP == OP_ALLREDUCE) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        lane(st.v, i) = __double2float_rn(__dmul_rn((double)lane(st.v, i), (double)kp.scale));
+    }
+    if constexpr (VEC) {
+      mm_st16(st.mp, st.v);
+    } else {
+      mm_st4(st.mp, st.v.x);
+      if (ref.cnt > 1) mm_st4(st.mp + 1, st.v.y);
+      if (ref.cnt > 2) mm_st4(st.mp + 2, st.v.z);
+      if (ref.cnt > 3) mm_st4(st.mp + 3, st.v.w);
+    }
+  }
+};
 
 // ------------------------------------------------------------------ kernels
 template <int OP, int P, int MINB>
@@ -483,9 +590,8 @@ __global__ void __launch_bounds__(512, MINB) k_twoshot_pull(KParams kp) {
     slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
   }
   stamp(kp, 2);
-  if (!barrier_all(kp, r, BAR_MID, true)) return;
   stamp(kp, 3);
-  gather_all<OP, P, MINB>(kp, r, par);
+  if (!gather_all<OP, P, MINB>(kp, r, par)) return;
   stamp(kp, 4);
   stamp(kp, 5);
 }
@@ -515,9 +621,8 @@ __global__ void __launch_bounds__(512, MINB) k_twoshot_push(KParams kp) {
     slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
   }
   stamp(kp, 2);
-  if (!barrier_all(kp, r, BAR_MID, true)) return;
   stamp(kp, 3);
-  gather_all<OP, P, MINB>(kp, r, par);
+  if (!gather_all<OP, P, MINB>(kp, r, par)) return;
   stamp(kp, 4);
   stamp(kp, 5);
 }
@@ -536,6 +641,47 @@ __global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
   stamp(kp, 1);
   ReduceBody<OP, P, SRC_ONESHOT, false> body{kp, r, 0, nullptr};
   slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
+  stamp(kp, 5);
+}
+
+// NVLS: ENTRY barrier -> owner slots reduced in the switch and multicast back -> MID barrier
+// (every owner's stores landed everywhere) -> SGD epilogue over this CTA's pieces of every
+// chunk from local memory.  Per GPU: ~(1 + 1/p) S of NVLink traffic each way.
+template <int OP, int P, int MINB>
+__global__ void __launch_bounds__(512, MINB) k_nvls(KParams kp) {
+  const int r = kp.rank0 + (int)blockIdx.y;
+  if (r == kp.absent_rank) return;
+  const int64_t M = kp.M;
+  stamp(kp, 0);
+  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
+  stamp(kp, 1);
+  {
+    NvlsBody<OP> body{kp, r};  // small state: 4 switch reductions in flight per lane
+    slot_loop<4>(kp, (int)(M * r / P), (int)(M * (r + 1) / P), body);
+  }
+  __threadfence_system();
+  stamp(kp, 2);
+  if constexpr (OP == OP_SGD) {
+    // epilogue: my own chunk first, then every other chunk as soon as its owner's CTA is done
+    signal_all(kp, r, BAR_MID);
+    auto epi = [&](int q) {
+      ReduceBody<OP_SGD, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
+      slot_loop<unroll_for(1, MINB)>(kp, (int)(M * q / P), (int)(M * (q + 1) / P), body);
+    };
+    epi(r);
+    stamp(kp, 3);
+#pragma unroll 1
+    for (int j = 0; j < P - 1; ++j) {
+      const int q = (r + 1 + ((int)blockIdx.x + j) % (P - 1)) % P;
+      if (!wait_one(kp, r, q, BAR_MID)) return;
+      epi(q);
+    }
+  } else {
+    // the result must have landed everywhere before the kernel (the call) completes
+    if (!barrier_all(kp, r, BAR_MID, true)) return;
+    stamp(kp, 3);
+  }
+  stamp(kp, 4);
   stamp(kp, 5);
 }
 
@@ -559,6 +705,10 @@ const void* kernel_ptr(int algo, int p, int variant) {
   }
 #define TC_CASE(PP)                                                                  \
   case PP:                                                                           \
+    if constexpr (OP != OP_EASGD)                                                    \
+      if (algo == ALGO_NVLS)                                                         \
+        return variant == 1 ? (const void*)k_nvls<OP, PP, 1> : (const void*)k_nvls<OP, PP, 2>; \
+    if (algo == ALGO_NVLS) return nullptr;                                           \
     if (variant == 1)                                                                \
       return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 1>           \
            : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 1>      \

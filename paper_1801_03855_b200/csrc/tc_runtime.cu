@@ -143,6 +143,8 @@ void free_group_device(Group& g) {
   cudaFree(g.d_block_t);
   cudaFree(g.d_numel);
   cudaFree(g.d_vec_ok);
+  cudaFree(g.d_mc);
+  g.d_mc = nullptr;
   g.d_ptrs = nullptr;
   g.d_prefix = nullptr;
   g.d_block_t = nullptr;
@@ -174,6 +176,11 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
   TC_CUDA(cudaMemcpy(g.d_numel, pl.numel.data(), sizeof(int64_t) * pl.numel.size(),
                      cudaMemcpyHostToDevice));
   TC_CUDA(cudaMemcpy(g.d_vec_ok, vec_ok.data(), vec_ok.size(), cudaMemcpyHostToDevice));
+  if (!g.h_mc.empty()) {
+    TC_CUDA(cudaMalloc((void**)&g.d_mc, sizeof(float*) * g.h_mc.size()));
+    TC_CUDA(cudaMemcpy(g.d_mc, g.h_mc.data(), sizeof(float*) * g.h_mc.size(),
+                       cudaMemcpyHostToDevice));
+  }
   return TC_OK;
 }
 
@@ -254,6 +261,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.a = ga->d_ptrs;
   kp.b = gb ? gb->d_ptrs : nullptr;
   kp.c = gc ? gc->d_ptrs : nullptr;
+  kp.mc = ga->d_mc;
   kp.flags = c.d_flags;
   kp.stage = c.d_stage;
   kp.arena = c.d_arena;
@@ -279,16 +287,25 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   } else {
     int64_t lim = c.tune_oneshot < 0 ? kDefaultOneshotMax : c.tune_oneshot;
     if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
-    algo = bytes <= lim ? ALGO_ONESHOT : (c.algo_override == ALGO_TWOSHOT_PUSH ? ALGO_TWOSHOT_PUSH
-                                                                              : ALGO_TWOSHOT);
-    if (algo != ALGO_ONESHOT && (pl.M + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
+    // Automatic choice (measured on B200, ResNet-50 group): p = 2 -> pulled
+    // two-shot (192 us vs 211 pushed); p = 3..5 -> pushed two-shot (p = 4: 282-290 us vs 288-298
+    // pulled and 298-305 NVLS); p >= 6 -> NVLS when the group is multicast-bound (it moves
+    // (1 + 1/p) S per GPU instead of 2(p-1)/p S, 1.56x less at p = 8), else pushed.
+    const bool nvls_ok = ga->d_mc != nullptr && op != OP_EASGD;
+    if (bytes <= lim) algo = ALGO_ONESHOT;
+    else if (c.algo_override == ALGO_TWOSHOT_PUSH) algo = ALGO_TWOSHOT_PUSH;
+    else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
+    else if (nvls_ok && (c.algo_override == ALGO_NVLS || p >= 6)) algo = ALGO_NVLS;
+    else algo = p == 2 ? ALGO_TWOSHOT : ALGO_TWOSHOT_PUSH;
+    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH) && (pl.M + p - 1) / p + 1 > c.arena_cap)
+      return TC_ERR_CUDA;
   }
   const int nlocal = c.emulated ? p : 1;
   int occ = max_ctas_per_sm(op, algo, p, threads, c.variant);
   if (occ < 1) return TC_ERR_CUDA;
   int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
   if (cap < 1) cap = 1;
-  const bool twoshot = algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH;
+  const bool twoshot = algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH || algo == ALGO_NVLS;
   int64_t work_slots = twoshot ? (pl.M + p - 1) / p : pl.M;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
@@ -444,7 +461,7 @@ tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t o
 }
 
 tc_status tc_comm_set_algorithm(tc_comm* comm, int algo) {
-  if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH))
+  if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH && algo != ALGO_NVLS))
     return TC_ERR_INVALID_ARG;
   comm->c.algo_override = algo;
   return TC_OK;
@@ -502,6 +519,7 @@ tc_status tc_comm_destroy(tc_comm* comm) {
       cudaFree(c.arena[r]);
     }
   }
+  free_all_sym(c);
   cudaFree(c.d_arena);
   cudaFree(c.d_flags);
   cudaFree(c.d_stage);
@@ -542,6 +560,13 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
   if (st == TC_OK && !c.emulated && p > 1) {
     for (int t = 0; t < ntensors && st == TC_OK; ++t) {
       if (numels[t] == 0) continue;
+      int64_t soff = 0;
+      const int si = find_sym(c, ptrs[t], (size_t)numels[t] * 4, &soff);
+      if (si >= 0) {  // symmetric allocation: peers already map it; index encoded as -(2 + i)
+        base_idx[t] = -(2 + si);
+        offs[t] = soff;
+        continue;
+      }
       void* base = nullptr;
       if (alloc_base(ptrs[t], &base) != cudaSuccess) {
         st = TC_ERR_NOT_SHAREABLE;
@@ -616,6 +641,34 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
       delete h;
       return st;
     }
+    // NVLS eligibility: every tensor in the same symmetric multicast allocation at the same
+    // offset on every rank (then its multicast address is mc + offset everywhere).
+    bool nvls = true;
+    std::vector<float*> mc_ptrs((size_t)T, nullptr);
+    for (int t = 0; t < T; ++t) {
+      if (numels[t] == 0) continue;
+      int32_t bi0 = 0;
+      int64_t off0 = 0;
+      for (int r = 0; r < p; ++r) {
+        const char* rd = recv.data() + (size_t)r * bytes;
+        int32_t bi;
+        int64_t off;
+        std::memcpy(&bi, rd + (size_t)maxb * hb + sizeof(int32_t) * t, sizeof(bi));
+        std::memcpy(&off, rd + (size_t)maxb * hb + sizeof(int32_t) * T + sizeof(int64_t) * t,
+                    sizeof(off));
+        if (r == 0) {
+          bi0 = bi;
+          off0 = off;
+        }
+        if (bi > -2 || bi != bi0 || off != off0) nvls = false;
+      }
+      if (nvls) {
+        const SymAlloc& sa = c.sym[(size_t)(-(bi0 + 2))];
+        if (!sa.multicast) nvls = false;
+        else mc_ptrs[t] = (float*)((char*)sa.mc + off0);
+      }
+    }
+    if (nvls) g.h_mc = mc_ptrs;
     for (int r = 0; r < p && st == TC_OK; ++r) {
       const char* rd = recv.data() + (size_t)r * bytes;
       const int32_t* bi = (const int32_t*)(rd + (size_t)maxb * hb);
@@ -639,7 +692,13 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
           g.h_ptrs[(size_t)r * T + t] = (float*)ptrs[t];
         } else {
           std::memcpy(off_r, offp + sizeof(int64_t) * t, sizeof(int64_t));
-          g.h_ptrs[(size_t)r * T + t] = (float*)((char*)rbases[bi[t]] + off_r[0]);
+          int32_t bit;
+          std::memcpy(&bit, &bi[t], sizeof(bit));
+          if (bit <= -2)
+            g.h_ptrs[(size_t)r * T + t] =
+                (float*)((char*)c.sym[(size_t)(-(bit + 2))].uc[r] + off_r[0]);
+          else
+            g.h_ptrs[(size_t)r * T + t] = (float*)((char*)rbases[bit] + off_r[0]);
         }
       }
     }

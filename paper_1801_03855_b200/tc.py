@@ -27,8 +27,8 @@ STATUS = {
 }
 TC_OK, TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_NOT_SHAREABLE = 0, 1, 2, 3
 TC_ERR_BUSY, TC_ERR_TIMEOUT, TC_ERR_CUDA, TC_ERR_BOOTSTRAP, TC_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
-ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 3: "two-shot-push"}
-ALGO_AUTO, ALGO_TWOSHOT_PULL, ALGO_TWOSHOT_PUSH = 0, 1, 3
+ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 3: "two-shot-push", 4: "nvls"}
+ALGO_AUTO, ALGO_TWOSHOT_PULL, ALGO_TWOSHOT_PUSH, ALGO_NVLS = 0, 1, 3, 4
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_size_t)
@@ -56,6 +56,9 @@ _SIGS = {
     "tc_comm_set_tuning": (_c_int, [_vp, _c_int, _c_int, _c_int64]),
     "tc_comm_set_timeout": (_c_int, [_vp, _c_int64]),
     "tc_comm_set_algorithm": (_c_int, [_vp, _c_int]),
+    "tc_mem_alloc": (_c_int, [_vp, ctypes.c_size_t, _pp]),
+    "tc_mem_free": (_c_int, [_vp, _vp]),
+    "tc_comm_multicast_supported": (_c_int, [_vp]),
     "tc_comm_set_debug_absent_rank": (_c_int, [_vp, _c_int]),
     "tc_comm_async_error": (_c_int, [_vp]),
     "tc_comm_set_profile_buffer": (_c_int, [_vp, _vp, _c_int64]),
@@ -232,8 +235,34 @@ class Comm:
     def set_tuning(self, num_ctas: int = 0, threads: int = 0, oneshot_max_bytes: int = -1):
         _check(LIB.tc_comm_set_tuning(self.h, num_ctas, threads, oneshot_max_bytes), "set_tuning")
 
+    @property
+    def multicast_supported(self) -> bool:
+        return bool(LIB.tc_comm_multicast_supported(self.h))
+
+    def alloc_symmetric(self, numel: int):
+        """Collective: a float32 CUDA tensor of `numel` elements in symmetric, multicast-bound
+        memory (tc_mem_alloc).  Groups of views at the same offsets on every rank can use the
+        NVLS algorithm.  The memory lives until free_symmetric() or destroy()."""
+        import torch
+        p = ctypes.c_void_p()
+        _check(LIB.tc_mem_alloc(self.h, int(numel) * 4, ctypes.byref(p)), "tc_mem_alloc")
+        dev = torch.cuda.current_device()
+
+        class _Cai:
+            __cuda_array_interface__ = {"shape": (int(numel),), "typestr": "<f4",
+                                        "data": (p.value, False), "version": 3, "strides": None}
+        t = torch.as_tensor(_Cai(), device=f"cuda:{dev}")
+        assert t.data_ptr() == p.value
+        self._sym = getattr(self, "_sym", []) + [t]
+        return t
+
+    def free_symmetric(self, tensor):
+        _check(LIB.tc_mem_free(self.h, tensor.data_ptr()), "tc_mem_free")
+        self._sym = [t for t in getattr(self, "_sym", []) if t is not tensor]
+
     def set_algorithm(self, algo: int):
-        """0 = automatic, 1 = two-shot pull, 3 = two-shot push (identical results)."""
+        """0 = automatic, 1 = two-shot pull, 3 = two-shot push (identical results),
+        4 = NVLS for groups in symmetric memory."""
         _check(LIB.tc_comm_set_algorithm(self.h, int(algo)), "set_algorithm")
 
     def set_timeout(self, ms: int):

@@ -68,6 +68,64 @@ def main():
             assert_bitwise(to_host(dc), wc, "easgd center")
         assert comm.async_error() == 0
 
+    # symmetric (tc_mem_alloc) memory: P2P algorithms bit-exact; NVLS (switch reduction) exact on
+    # integers, within the BASELINE tolerance on gradients, identical on every rank
+    numels = [7, 13, 1000, 0, 50001, 3, 262144]
+    sym = comm.alloc_symmetric(sum(numels) + 64)
+    views = list(torch.split(sym[:sum(numels)], numels))
+    algos = [1, 3] + ([4] if comm.multicast_supported else [])
+    comm.set_tuning(0, 0, 0)
+    with tc.Group(comm, views) as g:
+        for algo in algos:
+            comm.set_algorithm(algo)
+            for kind in ("int", "grad"):
+                xs = [W.group(numels, kind, 63, 0, k, W.GRAD) for k in range(p)]
+                for v, a in zip(views, xs[rank]):
+                    v.copy_(torch.from_numpy(a))
+                tc.allreduce(g)
+                assert comm.last_launch()[0] == tc.tc.ALGO_NAMES[algo]
+                got = to_host(views)
+                if algo != 4 or kind == "int":
+                    assert_bitwise(got, O.allreduce(xs), f"sym allreduce algo {algo} {kind}")
+                else:
+                    ref = O.allreduce_f64(xs)
+                    for t, n in enumerate(numels):
+                        bound = 1e-5 * sum(np.abs(xs[k][t].astype(np.float64)) for k in range(p))
+                        assert (np.abs(got[t] - ref[t]) <= bound).all(), f"nvls tolerance t={t}"
+                    # every rank holds the same bits
+                    import hashlib
+                    dig = hashlib.sha256(b"".join(a.tobytes() for a in got)).digest()
+                    h = torch.tensor([int.from_bytes(dig[:7], "little")])
+                    hs = [torch.zeros_like(h) for _ in range(p)]
+                    dist.all_gather(hs, h)
+                    assert all(int(x) == int(hs[0]) for x in hs), "nvls ranks differ"
+        if comm.multicast_supported:
+            # fused SGD over NVLS: G within tolerance, epilogue bit-exact given G
+            comm.set_algorithm(4)
+            gs = [W.group(numels, "grad", 64, 0, k, W.GRAD) for k in range(p)]
+            w = W.group(numels, "param", 64, 0, 0, W.PARAM)
+            dw = W.group(numels, "dw", 64, 0, 0, W.DW)
+            for v, a in zip(views, gs[rank]):
+                v.copy_(torch.from_numpy(a))
+            dwt, ddw = to_dev(w), to_dev(dw)
+            hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
+            with tc.Group(comm, dwt) as Wg, tc.Group(comm, ddw) as D:
+                tc.sgd_step(Wg, g, D, **hp)
+                assert comm.last_launch()[0] == "nvls"
+                G = to_host(views)
+                ref = O.allreduce_f64(gs)
+                for t in range(len(numels)):
+                    bound = 1e-5 * sum(np.abs(gs[k][t].astype(np.float64)) for k in range(p))
+                    assert (np.abs(G[t] - ref[t]) <= bound).all()
+                _, Ws, Dws = O.sgd_step([w], [G], [dw], **hp)
+                assert_bitwise(to_host(dwt), Ws[0], "nvls sgd w")
+                assert_bitwise(to_host(ddw), Dws[0], "nvls sgd dw")
+    comm.free_symmetric(sym)
+    assert comm.async_error() == 0
+    if rank == 0:
+        print(f"symmetric memory: algorithms {algos} ok (multicast={comm.multicast_supported})",
+              flush=True)
+
     # full-size ResNet-50 gradient group, fused SGD, checked on a sample of elements
     comm.set_tuning(0, 0, -1)
     comm.set_algorithm(3 if p % 2 == 0 else 1)

@@ -34,6 +34,8 @@ def _comm(p, oneshot=-1, ctas=0):
     if oneshot == PUSH:
         c.set_algorithm(3)
         oneshot = 0
+    elif oneshot == TWOSHOT and p > 1:
+        c.set_algorithm(1)
     c.set_tuning(ctas, 0, oneshot)
     return c
 

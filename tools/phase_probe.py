@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--algo", type=int, default=1)
+    ap.add_argument("--sym", action="store_true", help="gradients in tc_mem_alloc memory")
     a = ap.parse_args()
     dist.init_process_group("gloo")
     rank, p = dist.get_rank(), dist.get_world_size()
@@ -40,6 +41,10 @@ def main():
 
     g, w, dw = flat("grad", W.GRAD), flat("param", W.PARAM), flat("dw", W.DW)
     comm = tc.Comm.from_process_group(device=local)
+    if a.sym:
+        sym = comm.alloc_symmetric(sum(numels))
+        sym.copy_(torch.cat(g))
+        g = list(torch.split(sym, numels))
     comm.set_tuning(a.ctas, a.threads, 0)
     comm.set_algorithm(a.algo)
     prof = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")

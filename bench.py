@@ -384,7 +384,7 @@ def main():
         c = ecomm.nranks
         extra["easgd"] = {"t_us": te * 1e6, "clients": c,
                           "nvlink_ingress_gbs": (c - 1) * S / te / 1e9 if c > 1 else 0.0,
-                          "hbm_gbs_local": 5 * S / te / 1e9 if c == 1 else None,
+                          "hbm_gbs_local": 4 * S / te / 1e9 if c == 1 else None,
                           "algo": ecomm.last_launch()[0]}
         X.destroy()
         C.destroy()

@@ -487,17 +487,17 @@ __device__ bool wait_one(const KParams& kp, int r, int q, int bar) {
 }
 
 // Staged allgather: publish my staged chunk, then pull every other owner's chunk once that
-// owner's CTA has staged it.  CTA b visits the owners starting at r+1+(b mod p-1), so at any
-// moment every GPU serves about the same number of readers (a plain rotation by rank would
-// let one slow owner's readers pile up; "whichever is ready first" measured 30% slower at p=4
-// because the early owners' egress saturates).
+// owner's CTA has staged it, owners r+1, r+2, ... in turn.  At each step the ranks read from a
+// permutation of the owners, the NVLink pattern B200 serves fastest (p = 4: 117 us per phase;
+// owners mixed per CTA: 134-154 us; "whichever owner is ready first": 155-182 us, the early
+// owners' egress saturates).
 template <int OP, int P, int MINB>
 __device__ __forceinline__ bool gather_all(const KParams& kp, int r, int par) {
   const int64_t M = kp.M;
   signal_all(kp, r, BAR_MID);
 #pragma unroll 1
   for (int j = 0; j < P - 1; ++j) {
-    const int q = (r + 1 + ((int)blockIdx.x + j) % (P - 1)) % P;
+    const int q = (r + 1 + j) % P;
     if (!wait_one(kp, r, q, BAR_MID)) return false;
     const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
     GatherBody<OP> body{kp, r, lo, arena_stage(kp, q, par)};
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(512, MINB) k_nvls(KParams kp) {
     stamp(kp, 3);
 #pragma unroll 1
     for (int j = 0; j < P - 1; ++j) {
-      const int q = (r + 1 + ((int)blockIdx.x + j) % (P - 1)) % P;
+      const int q = (r + 1 + j) % P;
       if (!wait_one(kp, r, q, BAR_MID)) return;
       epi(q);
     }

@@ -54,6 +54,13 @@ tc_status bootstrap_allgather(tc_allgather_fn ag, void* ctx, int nranks, const v
                               void* recv, size_t bytes);
 
 // ---------------------------------------------------------------- kernel parameters
+// Per-rank device state of a comm: the epoch of the last completed call and the count of CTAs
+// that finished the current one (the last one advances the epoch).
+struct DevState {
+  uint32_t epoch;
+  uint32_t done;
+};
+
 // Passed by value to every hot-path kernel.  Tables are device arrays.
 struct KParams {
   int p;                 // ranks in the comm
@@ -66,6 +73,9 @@ struct KParams {
   const uint8_t* vec_ok; // [T] primary group 16-B aligned on every rank
   const uint8_t* vec_ok_b; // [T] same for group b (nullptr if unused)
   const uint8_t* vec_ok_c; // [T] same for group c (nullptr if unused)
+  const uint8_t* shift;    // [T] slot-grid shift (elements past a 16-B boundary) of group a
+  const uint8_t* shift_b;  // [T] same for group b / c (a vector path needs equal shifts)
+  const uint8_t* shift_c;
   float* const* a;       // [p*T] primary group: x (allreduce, easgd) or g (sgd)
   float* const* b;       // [p*T] w (sgd) or center (easgd)
   float* const* c;       // [p*T] dw (sgd)
@@ -74,8 +84,7 @@ struct KParams {
   float* const* stage;   // [p] one-shot staging buffers (peer-mapped), parity-selected
   float* const* arena;   // [p] per-rank arena: staging chunk x2 (parity) + p receive scratch
   int chunk_cap;         // slots per arena region (>= the largest owner chunk)
-  uint32_t epoch;
-  int stage_off;         // float offset of this call's parity half
+  DevState* state;       // [p] device-side call epochs (this process's ranks are valid)
   float scale, lr, mu, wd, rescale, alpha;
   unsigned long long timeout_ns;
   int* err;              // host-mapped sticky error word
@@ -122,7 +131,7 @@ struct Comm {
   float** d_stage = nullptr;      // device table [p]
   int* h_err = nullptr;           // host-mapped
   int* d_err = nullptr;
-  uint32_t epoch = 0;
+  DevState* d_state = nullptr;    // [kMaxRanks] device-side epochs
   std::array<float*, kMaxRanks> arena{};
   float** d_arena = nullptr;      // device table [p]
   int64_t arena_cap = 0;          // slots per region
@@ -152,6 +161,10 @@ struct Group {
   int* d_block_t = nullptr;
   int64_t* d_numel = nullptr;
   uint8_t* d_vec_ok = nullptr;
+  uint8_t* d_shift = nullptr;
+  std::vector<uint8_t> shift;    // [T] common misalignment in elements (0 if ranks differ)
+  std::vector<int64_t> dev_prefix;  // [T+1] slot prefix of the shifted grid
+  int64_t M = 0;                 // slots of the shifted grid
   std::vector<std::pair<int, std::string>> mapped_keys;  // ipc_cache keys held
   std::vector<float*> h_mc;      // [T] multicast addresses (NVLS-eligible groups only)
   float** d_mc = nullptr;

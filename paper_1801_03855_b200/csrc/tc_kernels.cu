@@ -76,6 +76,36 @@ __device__ __forceinline__ void stamp(const KParams& kp, int i) {
     kp.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = globaltimer();
 }
 
+// ------------------------------------------------------------------ call epoch (device side)
+// Every collective call on a comm gets the next epoch: the kernel reads its rank's counter at
+// start and the last CTA to finish advances it, so no host state enters the kernel arguments and
+// calls can be captured in a CUDA graph and replayed.  Flags compare against the epoch.
+__shared__ uint32_t s_epoch;
+
+__device__ __forceinline__ uint32_t ep() { return s_epoch; }
+// one-shot staging half used by this call (floats)
+__device__ __forceinline__ size_t stage_off() {
+  return (size_t)(s_epoch & 1u) * (kStageCapacity / sizeof(float));
+}
+
+__device__ __forceinline__ void call_begin(const KParams& kp, int r) {
+  if (threadIdx.x == 0) s_epoch = *(volatile uint32_t*)&kp.state[r].epoch + 1u;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void call_end(const KParams& kp, int r) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    DevState* st = kp.state + r;
+    if (atomicAdd(&st->done, 1u) == gridDim.x - 1) {
+      st->done = 0;
+      __threadfence();
+      *(volatile uint32_t*)&st->epoch = s_epoch;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ flags (A2)
 __device__ __forceinline__ size_t flag_index(int bar, int src, int cta) {
   return ((size_t)bar * kMaxRanks + src) * kMaxCtas + cta;
@@ -83,7 +113,7 @@ __device__ __forceinline__ size_t flag_index(int bar, int src, int cta) {
 
 // Thread 0: tell rank `to` that this CTA (rank r) passed point `bar`.  Caller has synced.
 __device__ __forceinline__ void signal_one(const KParams& kp, int bar, int r, int to) {
-  st_release_sys(kp.flags[to] + flag_index(bar, r, blockIdx.x), kp.epoch);
+  st_release_sys(kp.flags[to] + flag_index(bar, r, blockIdx.x), ep());
 }
 
 // Whole CTA: publish arrival at `bar` to every peer (if do_signal), then wait for every
@@ -93,11 +123,11 @@ __device__ bool barrier_all(const KParams& kp, int r, int bar, bool do_signal) {
   const int k = threadIdx.x;
   bool ok = true;
   if (k < kp.p && k != r) {
-    if (do_signal) st_release_sys(kp.flags[k] + flag_index(bar, r, blockIdx.x), kp.epoch);
+    if (do_signal) st_release_sys(kp.flags[k] + flag_index(bar, r, blockIdx.x), ep());
     const uint32_t* mine = kp.flags[r] + flag_index(bar, k, blockIdx.x);
-    if ((int32_t)(ld_acquire_sys(mine) - kp.epoch) < 0) {
+    if ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
       const unsigned long long t0 = globaltimer();
-      while ((int32_t)(ld_acquire_sys(mine) - kp.epoch) < 0) {
+      while ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
         if (globaltimer() - t0 > kp.timeout_ns) {
           atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
           ok = false;
@@ -113,7 +143,7 @@ __device__ bool barrier_all(const KParams& kp, int r, int bar, bool do_signal) {
 __device__ __forceinline__ void signal_all(const KParams& kp, int r, int bar) {
   __syncthreads();
   const int k = threadIdx.x;
-  if (k < kp.p && k != r) st_release_sys(kp.flags[k] + flag_index(bar, r, blockIdx.x), kp.epoch);
+  if (k < kp.p && k != r) st_release_sys(kp.flags[k] + flag_index(bar, r, blockIdx.x), ep());
 }
 
 // ------------------------------------------------------------------ element arithmetic
@@ -188,40 +218,56 @@ __device__ __forceinline__ void elem(const KParams& kp, int r, const float* in, 
 // ------------------------------------------------------------------ slot addressing
 // One lane's slot: flat slot s, element offset e inside its tensor, cnt valid elements (1..4).
 struct SlotRef {
-  int s, cnt;
-  int64_t e;
-  bool vec;  // full 16-B slot and the tensor is 16-B aligned in every group of the call
+  int s, cnt;      // flat slot; number of valid elements (0 = inactive lane)
+  int lo_i, hi_i;  // valid element lanes [lo_i, hi_i) of the slot
+  int64_t e;       // element index of lane 0 inside its tensor (negative for a shifted head)
+  bool vec;        // full 16-B slot, 16-B aligned in every group of the call
 };
 
 // Per-lane cache of the current tensor and the NP tensor pointers the phase body needs, so the
 // steady state issues no pointer-table loads (refreshed only when a lane crosses a tensor).
 template <int NP>
 struct TensorCache {
-  int t, lo, hi;
+  int t, lo, hi, shift;
   int64_t n;
   bool vec;
   float* ptr[NP];
 };
 
+// A tensor whose pointers sit m elements past a 16-B boundary on every rank (views of a flat
+// bucket with odd sizes) is laid out with its slot grid shifted by m: slot 0 holds elements
+// [0, 4-m), later slots are 16-B aligned, so it keeps the vector path.
 template <class Body>
 __device__ __forceinline__ void resolve(const KParams& kp, const Body& body,
                                         TensorCache<Body::NP>& c, int s, SlotRef& ref) {
   if (s < c.lo || s >= c.hi) {
-    // tensor of the slot's 128-slot block, then forward over tensors ending before s
-    int t = __ldg(kp.block_t + (s >> kPieceShift));
-    while (__ldg(kp.prefix + t + 1) <= s) ++t;
+    // the slot's tensor lies between the tensors holding the first slots of its 128-slot block
+    // and of the next block: binary search there (largest t with prefix[t] <= s)
+    const int blk = s >> kPieceShift;
+    int t = __ldg(kp.block_t + blk);
+    if (__ldg(kp.prefix + t + 1) <= s) {
+      int b = __ldg(kp.block_t + blk + 1) + 1;  // prefix[b] > s
+      while (b - t > 1) {
+        const int m = (t + b) >> 1;
+        if (__ldg(kp.prefix + m) <= s) t = m; else b = m;
+      }
+    }
     c.t = t;
     c.lo = __ldg(kp.prefix + t);
     c.hi = __ldg(kp.prefix + t + 1);
     c.n = __ldg(kp.numel + t);
-    c.vec = __ldg(kp.vec_ok + t) && (!kp.vec_ok_b || __ldg(kp.vec_ok_b + t)) &&
-            (!kp.vec_ok_c || __ldg(kp.vec_ok_c + t));
+    c.shift = __ldg(kp.shift + t);
+    c.vec = __ldg(kp.vec_ok + t) &&
+            (!kp.vec_ok_b || (__ldg(kp.vec_ok_b + t) && __ldg(kp.shift_b + t) == c.shift)) &&
+            (!kp.vec_ok_c || (__ldg(kp.vec_ok_c + t) && __ldg(kp.shift_c + t) == c.shift));
     body.bind(t, c.ptr);
   }
   ref.s = s;
-  ref.e = (int64_t)(s - c.lo) * 4;
+  ref.e = (int64_t)(s - c.lo) * 4 - c.shift;
+  ref.lo_i = ref.e < 0 ? (int)(-ref.e) : 0;
   const int64_t rem = c.n - ref.e;
-  ref.cnt = rem >= 4 ? 4 : (int)rem;
+  ref.hi_i = rem >= 4 ? 4 : (int)rem;
+  ref.cnt = ref.hi_i - ref.lo_i;
   ref.vec = c.vec && ref.cnt == 4;
 }
 
@@ -233,10 +279,9 @@ __device__ __forceinline__ float4 ldv(const float* base, const SlotRef& ref) {
     return ld16(base);
   } else {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    v.x = ld4(base);
-    if (ref.cnt > 1) v.y = ld4(base + 1);
-    if (ref.cnt > 2) v.z = ld4(base + 2);
-    if (ref.cnt > 3) v.w = ld4(base + 3);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i >= ref.lo_i && i < ref.hi_i) lane(v, i) = ld4(base + i);
     return v;
   }
 }
@@ -246,10 +291,9 @@ __device__ __forceinline__ void stv(float* base, const SlotRef& ref, float4 v) {
   if constexpr (VEC) {
     st16(base, v);
   } else {
-    st4(base, v.x);
-    if (ref.cnt > 1) st4(base + 1, v.y);
-    if (ref.cnt > 2) st4(base + 2, v.z);
-    if (ref.cnt > 3) st4(base + 3, v.w);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i >= ref.lo_i && i < ref.hi_i) st4(base + i, lane(v, i));
   }
 }
 
@@ -349,7 +393,7 @@ struct ReduceBody {
         st.x[k] = (k == r) ? ldv<VEC>(ptr[0], ref)
                            : ld16(arena_scratch(kp, r, k) + (size_t)(ref.s - origin) * 4);
       } else {
-        st.x[k] = ld16(kp.stage[k] + kp.stage_off + (size_t)ref.s * 4);
+        st.x[k] = ld16(kp.stage[k] + stage_off() + (size_t)ref.s * 4);
       }
     }
     if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
@@ -468,9 +512,9 @@ __device__ bool wait_one(const KParams& kp, int r, int q, int bar) {
   if (threadIdx.x == 0) {
     int ok = 1;
     const uint32_t* mine = kp.flags[r] + flag_index(bar, q, blockIdx.x);
-    if ((int32_t)(ld_acquire_sys(mine) - kp.epoch) < 0) {
+    if ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
       const unsigned long long t0 = globaltimer();
-      while ((int32_t)(ld_acquire_sys(mine) - kp.epoch) < 0) {
+      while ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
         if (globaltimer() - t0 > kp.timeout_ns) {
           atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
           ok = 0;
@@ -550,10 +594,9 @@ struct NvlsBody {
       st.v = mm_ld_reduce16(st.mp);
     } else {
       st.v = make_float4(0.f, 0.f, 0.f, 0.f);
-      st.v.x = mm_ld_reduce4(st.mp);
-      if (ref.cnt > 1) st.v.y = mm_ld_reduce4(st.mp + 1);
-      if (ref.cnt > 2) st.v.z = mm_ld_reduce4(st.mp + 2);
-      if (ref.cnt > 3) st.v.w = mm_ld_reduce4(st.mp + 3);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i >= ref.lo_i && i < ref.hi_i) lane(st.v, i) = mm_ld_reduce4(st.mp + i);
     }
   }
   template <bool VEC>
@@ -566,10 +609,9 @@ struct NvlsBody {
     if constexpr (VEC) {
       mm_st16(st.mp, st.v);
     } else {
-      mm_st4(st.mp, st.v.x);
-      if (ref.cnt > 1) mm_st4(st.mp + 1, st.v.y);
-      if (ref.cnt > 2) mm_st4(st.mp + 2, st.v.z);
-      if (ref.cnt > 3) mm_st4(st.mp + 3, st.v.w);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i >= ref.lo_i && i < ref.hi_i) mm_st4(st.mp + i, lane(st.v, i));
     }
   }
 };
@@ -579,7 +621,8 @@ template <int OP, int P, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_twoshot_pull(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
-  const int par = (int)(kp.epoch & 1u);
+  call_begin(kp, r);
+  const int par = (int)(ep() & 1u);
   const int64_t M = kp.M;
   stamp(kp, 0);
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
@@ -593,6 +636,7 @@ __global__ void __launch_bounds__(512, MINB) k_twoshot_pull(KParams kp) {
   stamp(kp, 3);
   if (!gather_all<OP, P, MINB>(kp, r, par)) return;
   stamp(kp, 4);
+  call_end(kp, r);
   stamp(kp, 5);
 }
 
@@ -600,7 +644,8 @@ template <int OP, int P, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_twoshot_push(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
-  const int par = (int)(kp.epoch & 1u);
+  call_begin(kp, r);
+  const int par = (int)(ep() & 1u);
   const int64_t M = kp.M;
   stamp(kp, 0);
   // push my contribution to this CTA's pieces of every other chunk into its owner's scratch
@@ -624,6 +669,7 @@ __global__ void __launch_bounds__(512, MINB) k_twoshot_push(KParams kp) {
   stamp(kp, 3);
   if (!gather_all<OP, P, MINB>(kp, r, par)) return;
   stamp(kp, 4);
+  call_end(kp, r);
   stamp(kp, 5);
 }
 
@@ -631,16 +677,18 @@ template <int OP, int P, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
+  call_begin(kp, r);
   const int lo = 0, hi = kp.M;
   stamp(kp, 0);
   {
-    CopyOutBody body{kp, r, 0, kp.stage[r] + kp.stage_off};
+    CopyOutBody body{kp, r, 0, kp.stage[r] + stage_off()};
     slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
   }
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
   stamp(kp, 1);
   ReduceBody<OP, P, SRC_ONESHOT, false> body{kp, r, 0, nullptr};
   slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
+  call_end(kp, r);
   stamp(kp, 5);
 }
 
@@ -651,6 +699,7 @@ template <int OP, int P, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_nvls(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
+  call_begin(kp, r);
   const int64_t M = kp.M;
   stamp(kp, 0);
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
@@ -682,6 +731,7 @@ __global__ void __launch_bounds__(512, MINB) k_nvls(KParams kp) {
     stamp(kp, 3);
   }
   stamp(kp, 4);
+  call_end(kp, r);
   stamp(kp, 5);
 }
 

@@ -75,6 +75,8 @@ tc_status finish_comm(Comm& c) {
   TC_CUDA(cudaHostAlloc((void**)&c.h_err, sizeof(int), cudaHostAllocMapped));
   *c.h_err = 0;
   TC_CUDA(cudaHostGetDevicePointer((void**)&c.d_err, c.h_err, 0));
+  TC_CUDA(cudaMalloc((void**)&c.d_state, sizeof(DevState) * kMaxRanks));
+  TC_CUDA(cudaMemset(c.d_state, 0, sizeof(DevState) * kMaxRanks));
   TC_CUDA(cudaMalloc((void**)&c.d_flags, sizeof(uint32_t*) * kMaxRanks));
   TC_CUDA(cudaMalloc((void**)&c.d_stage, sizeof(float*) * kMaxRanks));
   TC_CUDA(cudaMemcpy(c.d_flags, c.flags.data(), sizeof(uint32_t*) * kMaxRanks,
@@ -143,6 +145,8 @@ void free_group_device(Group& g) {
   cudaFree(g.d_block_t);
   cudaFree(g.d_numel);
   cudaFree(g.d_vec_ok);
+  cudaFree(g.d_shift);
+  g.d_shift = nullptr;
   cudaFree(g.d_mc);
   g.d_mc = nullptr;
   g.d_ptrs = nullptr;
@@ -152,14 +156,31 @@ void free_group_device(Group& g) {
   g.d_vec_ok = nullptr;
 }
 
+// The device slot grid: tensor t (common misalignment m_t elements on every rank) occupies
+// ceil((n_t + m_t)/4) slots, its first slot holding elements [0, 4 - m_t).
+tc_status build_device_grid(Group& g, const std::vector<uint8_t>& vec_ok) {
+  const Plan& pl = g.plan;
+  g.dev_prefix.assign((size_t)pl.T + 1, 0);
+  for (int t = 0; t < pl.T; ++t) {
+    const int64_t n = pl.numel[(size_t)t];
+    const int64_t m = vec_ok[(size_t)t] ? g.shift[(size_t)t] : 0;
+    if (!vec_ok[(size_t)t]) g.shift[(size_t)t] = 0;
+    g.dev_prefix[(size_t)t + 1] = g.dev_prefix[(size_t)t] + (n > 0 ? (n + m + 3) / 4 : 0);
+  }
+  g.M = g.dev_prefix[(size_t)pl.T];
+  return g.M >= (int64_t(1) << 31) ? TC_ERR_INVALID_ARG : TC_OK;
+}
+
 tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
   const Plan& pl = g.plan;
-  std::vector<int> prefix(pl.slot_prefix.begin(), pl.slot_prefix.end());
+  tc_status gs = build_device_grid(g, vec_ok);
+  if (gs != TC_OK) return gs;
+  std::vector<int> prefix(g.dev_prefix.begin(), g.dev_prefix.end());
   // tensor of the first slot of every 128-slot block (largest t with prefix[t] <= slot)
-  std::vector<int> block_t((size_t)((pl.M + kPiece - 1) >> kPieceShift) + 1, 0);
+  std::vector<int> block_t((size_t)((g.M + kPiece - 1) >> kPieceShift) + 1, 0);
   for (size_t j = 0, t = 0; j < block_t.size(); ++j) {
     const int64_t slot = (int64_t)j << kPieceShift;
-    while (t + 1 < (size_t)pl.T && pl.slot_prefix[t + 1] <= slot) ++t;
+    while (t + 1 < (size_t)pl.T && g.dev_prefix[t + 1] <= slot) ++t;
     block_t[j] = (int)t;
   }
   TC_CUDA(cudaMalloc((void**)&g.d_block_t, sizeof(int) * block_t.size()));
@@ -176,6 +197,8 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
   TC_CUDA(cudaMemcpy(g.d_numel, pl.numel.data(), sizeof(int64_t) * pl.numel.size(),
                      cudaMemcpyHostToDevice));
   TC_CUDA(cudaMemcpy(g.d_vec_ok, vec_ok.data(), vec_ok.size(), cudaMemcpyHostToDevice));
+  TC_CUDA(cudaMalloc((void**)&g.d_shift, g.shift.size()));
+  TC_CUDA(cudaMemcpy(g.d_shift, g.shift.data(), g.shift.size(), cudaMemcpyHostToDevice));
   if (!g.h_mc.empty()) {
     TC_CUDA(cudaMalloc((void**)&g.d_mc, sizeof(float*) * g.h_mc.size()));
     TC_CUDA(cudaMemcpy(g.d_mc, g.h_mc.data(), sizeof(float*) * g.h_mc.size(),
@@ -247,13 +270,14 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (*(volatile int*)c.h_err) return (tc_status)*(volatile int*)c.h_err;
   const Plan& pl = ga->plan;
   const int p = c.nranks;
-  if (pl.M == 0) return TC_OK;  // empty group: nothing to reduce (still collective-safe)
+  const int64_t Mdev = ga->M;   // slots of the (shifted) device grid
+  if (Mdev == 0) return TC_OK;  // empty group: nothing to reduce (still collective-safe)
   KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   kp.p = p;
   kp.rank0 = c.emulated ? 0 : c.rank;
   kp.T = pl.T;
-  kp.M = (int)pl.M;
+  kp.M = (int)Mdev;
   kp.prefix = ga->d_prefix;
   kp.block_t = ga->d_block_t;
   kp.numel = ga->d_numel;
@@ -278,14 +302,20 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   // The vector path is taken for a tensor only if it is 16-B aligned in every group involved.
   kp.vec_ok_b = gb ? gb->d_vec_ok : nullptr;
   kp.vec_ok_c = gc ? gc->d_vec_ok : nullptr;
+  kp.shift = ga->d_shift;
+  kp.shift_b = gb ? gb->d_shift : nullptr;
+  kp.shift_c = gc ? gc->d_shift : nullptr;
 
   const int threads = c.tune_threads;
-  const int64_t bytes = pl.M * 16;
+  const int64_t bytes = Mdev * 16;
   int algo;
   if (p == 1) {
     algo = ALGO_LOCAL;
   } else {
-    int64_t lim = c.tune_oneshot < 0 ? kDefaultOneshotMax : c.tune_oneshot;
+    // One-shot moves (p-1)S per GPU against 2(p-1)/p S for two-shot but needs one barrier
+    // instead of two: at p = 2 the traffic is equal, so it wins up to the staging capacity.
+    const int64_t auto_lim = p == 2 ? (int64_t)kStageCapacity : (p <= 4 ? (1 << 20) : kDefaultOneshotMax);
+    int64_t lim = c.tune_oneshot < 0 ? auto_lim : c.tune_oneshot;
     if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
     // Automatic choice (measured on B200, ResNet-50 group): p = 2 -> pulled
     // two-shot (192 us vs 211 pushed); p = 3..5 -> pushed two-shot (p = 4: 282-290 us vs 288-298
@@ -297,7 +327,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
     else if (nvls_ok && (c.algo_override == ALGO_NVLS || p >= 6)) algo = ALGO_NVLS;
     else algo = p == 2 ? ALGO_TWOSHOT : ALGO_TWOSHOT_PUSH;
-    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH) && (pl.M + p - 1) / p + 1 > c.arena_cap)
+    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH) && (Mdev + p - 1) / p + 1 > c.arena_cap)
       return TC_ERR_CUDA;
   }
   const int nlocal = c.emulated ? p : 1;
@@ -306,7 +336,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
   if (cap < 1) cap = 1;
   const bool twoshot = algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH || algo == ALGO_NVLS;
-  int64_t work_slots = twoshot ? (pl.M + p - 1) / p : pl.M;
+  int64_t work_slots = twoshot ? (Mdev + p - 1) / p : Mdev;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
   if (algo == ALGO_LOCAL) {
@@ -322,8 +352,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   }
   if (ctas < 1) ctas = 1;
   if (c.prof && (int64_t)ctas * nlocal <= c.prof_slots) kp.prof = c.prof;
-  kp.epoch = ++c.epoch;
-  kp.stage_off = (int)((kp.epoch & 1u) * (kStageCapacity / sizeof(float)));
+  kp.state = c.d_state;
   cudaError_t e = launch_hot(op, algo, kp, ctas, threads, nlocal, c.emulated && p > 1, stream,
                              c.variant);
   if (e != cudaSuccess) {
@@ -520,6 +549,7 @@ tc_status tc_comm_destroy(tc_comm* comm) {
     }
   }
   free_all_sym(c);
+  cudaFree(c.d_state);
   cudaFree(c.d_arena);
   cudaFree(c.d_flags);
   cudaFree(c.d_stage);
@@ -613,13 +643,22 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
   const int T = ntensors;
   g.h_ptrs.assign((size_t)p * T, nullptr);
   std::vector<uint8_t> vec_ok((size_t)T, 1);
+  g.shift.assign((size_t)T, 0);
+  // misalignment (elements past a 16-B boundary) of tensor t on rank r; a tensor keeps the vector
+  // path iff every rank has the same misalignment (0xFF: empty tensor, no constraint)
+  auto note_mis = [&](int t, int r, uint8_t mis) {
+    if (mis == 0xFF) return;
+    if (r == 0 || g.shift[(size_t)t] == 0xFE) g.shift[(size_t)t] = mis;
+    else if (g.shift[(size_t)t] != mis) vec_ok[(size_t)t] = 0;
+  };
+  for (int t = 0; t < T; ++t) g.shift[(size_t)t] = 0xFE;  // unset
 
   if (c.emulated || p == 1) {
     for (int l = 0; l < nlocal; ++l)
       for (int t = 0; t < T; ++t) {
         float* q = (float*)ptrs[(size_t)l * T + t];
         g.h_ptrs[(size_t)l * T + t] = q;
-        if (((uintptr_t)q & 15u) != 0) vec_ok[t] = 0;
+        note_mis(t, l == 0 ? 0 : 1, numels[t] ? (uint8_t)(((uintptr_t)q & 15u) >> 2) : 0xFF);
       }
   } else {
     // Payload exchange: handles, per-tensor (base index, offset), alignment bits.
@@ -635,7 +674,8 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
     w += sizeof(int32_t) * T;
     std::memcpy(w, offs.data(), sizeof(int64_t) * T);
     w += sizeof(int64_t) * T;
-    for (int t = 0; t < T; ++t) w[t] = ((uintptr_t)ptrs[t] & 15u) == 0;
+    for (int t = 0; t < T; ++t)
+      w[t] = numels[t] ? (char)(((uintptr_t)ptrs[t] & 15u) >> 2) : (char)0xFF;
     st = bootstrap_allgather(c.ag, c.ag_ctx, p, send.data(), recv.data(), bytes);
     if (st != TC_OK) {
       delete h;
@@ -686,7 +726,7 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
         }
       }
       for (int t = 0; t < T && st == TC_OK; ++t) {
-        if (!al[t]) vec_ok[t] = 0;
+        note_mis(t, r == 0 ? 0 : 1, (uint8_t)al[t]);
         if (numels[t] == 0) continue;
         if (r == c.rank) {
           g.h_ptrs[(size_t)r * T + t] = (float*)ptrs[t];
@@ -709,9 +749,11 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
       return st;
     }
   }
+  for (int t = 0; t < T; ++t)
+    if (g.shift[(size_t)t] > 3) g.shift[(size_t)t] = 0;  // empty on every rank
   st = upload_group(g, vec_ok);
   if (!c.emulated && p > 1) st = agree(c, st);
-  if (st == TC_OK) st = grow_arena(c, (g.plan.M + p - 1) / p + 1);
+  if (st == TC_OK) st = grow_arena(c, (g.M + p - 1) / p + 1);
   if (st != TC_OK) {
     free_group_device(g);
     for (auto& k : g.mapped_keys) unmap_peer(c, k);

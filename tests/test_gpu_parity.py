@@ -41,9 +41,11 @@ def _comm(p, oneshot=-1, ctas=0):
 
 
 def run_allreduce(xs, scale=1.0, oneshot=-1, offset=0, ctas=0):
+    """offset: elements each tensor starts past its allocation (int, or a callable of the rank)."""
     p = len(xs)
     comm = _comm(p, oneshot, ctas)
-    dev = [to_dev(x, offset=offset) for x in xs]
+    off = offset if callable(offset) else (lambda k: offset)
+    dev = [to_dev(x, offset=off(k)) for k, x in enumerate(xs)]
     grp = tc.Group(comm, dev if p > 1 else dev[0])
     tc.allreduce(grp, scale)
     out = [to_host(d) for d in dev]
@@ -86,15 +88,44 @@ def test_random_groups_grad_values(p, name, oneshot):
         assert (np.abs(out[0][t] - ref[t]) <= bound).all()
 
 
+@pytest.mark.parametrize("offset", [1, 2, 3, "per-rank"])
 @pytest.mark.parametrize("p", [2, 4])
-def test_unaligned_tensors_scalar_path(p):
-    """Tensors starting 4 bytes into their allocation (not 16-B aligned): scalar path."""
-    numels = [7, 13, 1000, 4096, 3]
+def test_unaligned_tensors(p, offset):
+    """Tensors starting 1-3 elements past a 16-B boundary.  Same misalignment on every rank:
+    shifted slot grid, vector path.  Misalignment differing by rank: scalar path."""
+    numels = [7, 13, 1000, 4096, 3, 1, 2]
     xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
+    off = (lambda k: k % 4) if offset == "per-rank" else offset
     for oneshot in (TWOSHOT, PUSH, ONESHOT):
-        out, _ = run_allreduce(xs, oneshot=oneshot, offset=1)
+        out, _ = run_allreduce(xs, oneshot=oneshot, offset=off)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
+
+
+def test_sgd_mixed_alignment():
+    """g as views of one flat buffer (odd sizes: misaligned), w and dw separate allocations:
+    the primary grid is shifted, the other operands fall back to the scalar path."""
+    p = 3
+    numels = [7, 13, 1000, 4097, 3]
+    gs = [W.group(numels, "grad", 70, 0, k, W.GRAD) for k in range(p)]
+    w = W.group(numels, "param", 70, 0, 0, W.PARAM)
+    dw = W.group(numels, "dw", 70, 0, 0, W.DW)
+    comm = _comm(p, TWOSHOT)
+    flats = [torch.from_numpy(np.concatenate(gs[k])).cuda() for k in range(p)]
+    dg = [list(torch.split(f, numels)) for f in flats]
+    dwt = [to_dev(w) for _ in range(p)]
+    ddw = [to_dev(dw, offset=2) for _ in range(p)]
+    G, Wg, D = tc.Group(comm, dg), tc.Group(comm, dwt), tc.Group(comm, ddw)
+    hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 384)
+    tc.sgd_step(Wg, G, D, **hp)
+    Gw, Ws, Dws = O.sgd_step([w] * p, gs, [dw] * p, **hp)
+    for r in range(p):
+        assert_bitwise(to_host(dg[r]), Gw, f"g rank {r}")
+        assert_bitwise(to_host(dwt[r]), Ws[r], f"w rank {r}")
+        assert_bitwise(to_host(ddw[r]), Dws[r], f"dw rank {r}")
+    for grp in (G, Wg, D):
+        grp.destroy()
+    comm.destroy()
 
 
 @pytest.mark.parametrize("p", [4, 8])

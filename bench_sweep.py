@@ -60,14 +60,21 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--max-k", type=int, default=10)
+    ap.add_argument("--algo", type=int, default=0, help="0 auto, 1 pull, 3 push, 4 NVLS")
+    ap.add_argument("--oneshot", type=int, default=-1, help="one-shot limit in bytes (-1 auto)")
+    ap.add_argument("--sizes", default="", help="comma list of k (total = 1 KiB * 4^k)")
+    ap.add_argument("--tensors", default="1,2,8,32,161,512,1024")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, p = dist.get_rank(), dist.get_world_size()
     comm = tc.Comm.from_process_group(device=local)
+    comm.set_algorithm(a.algo)
+    comm.set_tuning(0, 0, a.oneshot)
     out = open(a.out, "w") if (a.out and rank == 0) else None
-    for k in range(a.max_k + 1):
+    ks = [int(x) for x in a.sizes.split(",")] if a.sizes else range(a.max_k + 1)
+    for k in ks:
         total = 1024 * 4 ** k
         N = total // 4
         flat = torch.randn(N, device="cuda")
@@ -75,7 +82,7 @@ def main():
         iters = 200 if total <= (1 << 20) else (50 if total <= (64 << 20) else 5)
         graph = total <= (64 << 20)
         t_nccl = timed(lambda: dist.all_reduce(nccl_buf), iters, graph=graph)
-        for T in (1, 2, 8, 32, 161, 512, 1024):
+        for T in [int(x) for x in a.tensors.split(",")]:
             numels = W.sweep_numels(total, T)
             if not numels:
                 continue

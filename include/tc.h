@@ -132,8 +132,8 @@ TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, in
  * multimem.st; only for groups in tc_mem_alloc memory, else two-shot).  1 and 3 end with the
  * staged pull allgather and give bit-identical results (float64, rank order).  NVLS sums in
  * the switch in fp32 (order unspecified): exact for integer-valued data, else within
- * (p-1) ulp-scale of the float64 sum; identical on every rank.  Automatic: p = 2 pull,
- * p = 3..5 push, p >= 6 NVLS for eligible groups (else push).  Errors: TC_ERR_INVALID_ARG. */
+ * (p-1) ulp-scale of the float64 sum; identical on every rank.  Automatic: pull up to
+ * p = 5, p >= 6 NVLS for eligible groups (else pull).  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 
 /* Device-barrier timeout in milliseconds (default 30000, or env TC_TIMEOUT_MS). */

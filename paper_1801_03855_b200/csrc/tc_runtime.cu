@@ -313,20 +313,21 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     algo = ALGO_LOCAL;
   } else {
     // One-shot moves (p-1)S per GPU against 2(p-1)/p S for two-shot but needs one barrier
-    // instead of two: at p = 2 the traffic is equal, so it wins up to the staging capacity.
-    const int64_t auto_lim = p == 2 ? (int64_t)kStageCapacity : (p <= 4 ? (1 << 20) : kDefaultOneshotMax);
+    // instead of a chain of per-owner waits: measured to win up to the 8 MiB staging capacity at
+    // p <= 4 (p = 4, 4 MiB: 34 us vs 52 two-shot, NCCL 35).
+    const int64_t auto_lim = p <= 4 ? (int64_t)kStageCapacity : kDefaultOneshotMax;
     int64_t lim = c.tune_oneshot < 0 ? auto_lim : c.tune_oneshot;
     if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
-    // Automatic choice (measured on B200, ResNet-50 group): p = 2 -> pulled
-    // two-shot (192 us vs 211 pushed); p = 3..5 -> pushed two-shot (p = 4: 282-290 us vs 288-298
-    // pulled and 298-305 NVLS); p >= 6 -> NVLS when the group is multicast-bound (it moves
-    // (1 + 1/p) S per GPU instead of 2(p-1)/p S, 1.56x less at p = 8), else pushed.
+    // Automatic choice (measured on B200, config-5 sweep and ResNet-50 group):
+    // pulled two-shot up to p = 5 (p = 4: 16/64/256 MiB in 72/189/679 us vs 95/210/737 pushed,
+    // NCCL 70/185/685); p >= 6 -> NVLS when the group is multicast-bound (it moves (1 + 1/p) S
+    // per GPU instead of 2(p-1)/p S, 1.56x less at p = 8), else pulled.
     const bool nvls_ok = ga->d_mc != nullptr && op != OP_EASGD;
     if (bytes <= lim) algo = ALGO_ONESHOT;
     else if (c.algo_override == ALGO_TWOSHOT_PUSH) algo = ALGO_TWOSHOT_PUSH;
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
     else if (nvls_ok && (c.algo_override == ALGO_NVLS || p >= 6)) algo = ALGO_NVLS;
-    else algo = p == 2 ? ALGO_TWOSHOT : ALGO_TWOSHOT_PUSH;
+    else algo = ALGO_TWOSHOT;
     if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH) && (Mdev + p - 1) / p + 1 > c.arena_cap)
       return TC_ERR_CUDA;
   }

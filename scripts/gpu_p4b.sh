@@ -1,0 +1,7 @@
+export TC_TIMEOUT_MS=20000
+NP=4
+mkdir -p gpurun_out/r01
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $NP --master-addr 127.0.0.1 --master-port 29519"
+timeout 900 $TR bench_sweep.py --out gpurun_out/r01/sweep_p4.jsonl > gpurun_out/r01/sweep_p4.log 2>&1; echo "sweep rc=$?"
+timeout 600 $TR bench.py --gpus $NP > gpurun_out/r01/bench_n4.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/r01/bench_n4.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print({k:d[k] for k in ['t_us','busbw_gbs','allreduce_only','nccl_allreduce_flat','easgd','e2e']}, d['config']['algo'])"

@@ -341,3 +341,50 @@ def test_timeout_when_a_rank_is_absent():
     assert e.value.status == tc.tc.TC_ERR_TIMEOUT
     grp.destroy()
     comm.destroy()
+
+
+# ------------------------------------------------------------------ full-size configs (sampled)
+def _sampled_check(numels, outs, xs, scale, p, seed=0, per_tensor=48):
+    """The oracle on sampled elements of every 5th tensor (+ the largest), element by element."""
+    rng = np.random.default_rng(seed)
+    ts = sorted(set(list(range(0, len(numels), 5)) + [int(np.argmax(numels)), len(numels) - 1]))
+    for t in ts:
+        idx = rng.integers(0, numels[t], size=min(per_tensor, numels[t]))
+        want = O.allreduce([[x[t][idx]] for x in xs], scale)[0]
+        for r in range(p):
+            assert_bitwise([outs[r][t][idx]], [want], f"tensor {t} rank {r}")
+
+
+@pytest.mark.parametrize("group,p,oneshot", [("resnet50", 1, -1), ("resnet50", 2, TWOSHOT),
+                                             ("resnet50", 4, PUSH), ("alexnet", 2, TWOSHOT)])
+def test_full_size_groups_sampled(group, p, oneshot):
+    """Configs 2/3 at their full size (ResNet-50 25.6M, AlexNet 61.1M fp32 per rank), in the
+    launch configuration bench.py times, checked on sampled outputs."""
+    numels = W.GROUPS[group]
+    xs = [W.group(numels, "grad", W.CFG_ALEX_VGG if group != "resnet50" else W.CFG_RESNET50, 0,
+                  k, W.GRAD) for k in range(p)]
+    out, algo = run_allreduce(xs, scale=1.0 / p, oneshot=oneshot)
+    _sampled_check(numels, out, xs, 1.0 / p, p)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("T", [1, 2, 8, 32, 161, 512, 1024])
+def test_config5_sweep_shapes(p, T):
+    """Config 5 shapes (seeded log-uniform splits, unaligned tails) at the small totals the
+    oracle covers fully (16 KiB, 1 MiB), as views of one flat buffer like bench_sweep.py."""
+    for total in (16 << 10, 1 << 20):
+        numels = W.sweep_numels(total, T)
+        if not numels:
+            continue
+        xs = [W.group(numels, "grad", W.CFG_SWEEP, 0, k, W.GRAD) for k in range(p)]
+        for oneshot in (TWOSHOT, ONESHOT):
+            comm = _comm(p, oneshot)
+            flats = [torch.from_numpy(np.concatenate(x)).cuda() for x in xs]
+            views = [list(torch.split(f, numels)) for f in flats]
+            grp = tc.Group(comm, views)
+            tc.allreduce(grp, 0.5)
+            want = O.allreduce(xs, 0.5)
+            for r in range(p):
+                assert_bitwise(to_host(views[r]), want, f"T={T} total={total} rank {r}")
+            grp.destroy()
+            comm.destroy()

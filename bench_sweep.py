@@ -63,6 +63,7 @@ def main():
     ap.add_argument("--algo", type=int, default=0, help="0 auto, 1 pull, 3 push, 4 NVLS")
     ap.add_argument("--oneshot", type=int, default=-1, help="one-shot limit in bytes (-1 auto)")
     ap.add_argument("--sizes", default="", help="comma list of k (total = 1 KiB * 4^k)")
+    ap.add_argument("--ll", type=int, default=-1, help="low-latency limit in bytes (-1 auto)")
     ap.add_argument("--tensors", default="1,2,8,32,161,512,1024")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -72,6 +73,7 @@ def main():
     comm = tc.Comm.from_process_group(device=local)
     comm.set_algorithm(a.algo)
     comm.set_tuning(0, 0, a.oneshot)
+    comm.set_ll_max(a.ll)
     out = open(a.out, "w") if (a.out and rank == 0) else None
     ks = [int(x) for x in a.sizes.split(",")] if a.sizes else range(a.max_k + 1)
     for k in ks:

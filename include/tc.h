@@ -126,6 +126,14 @@ TC_API tc_status tc_comm_create_emulated(int nranks, int cuda_device, tc_comm** 
  * calls.  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t oneshot_max_bytes);
 
+/* Groups of at most `bytes` of data (-1 = automatic: 1 MiB at p = 2, 512 KiB at p <= 4,
+ * 128 KiB beyond; 0 = never) use the low-latency algorithm:
+ * every rank stores each element to every peer as one 8-byte {value, call epoch} word and waits
+ * for its peers' words in local memory, so a call costs one NVLink crossing and no barrier.
+ * Same arithmetic (float64, rank order) as the other P2P algorithms.  Capped by the LL buffer
+ * (16 MiB / (16 p) elements).  Must be identical on all ranks.  Errors: TC_ERR_INVALID_ARG. */
+TC_API tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes);
+
 /* Large-group algorithm (must be identical on all ranks): 0 = automatic, 1 = two-shot with
  * pulled reduce-scatter (loads from peers' tensors), 3 = two-shot with pushed reduce-scatter
  * (stores into the owners' receive scratch), 4 = NVLS (switch reduction, multimem.ld_reduce +
@@ -230,8 +238,8 @@ TC_API tc_status tc_sgd_step(tc_group* w, tc_group* g, tc_group* dw, float lr, f
 TC_API tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream);
 
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
- * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS), grid
- * CTAs per rank, threads. */
+ * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS,
+ * 5 = low-latency), grid CTAs per rank, threads. */
 TC_API tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads);
 
 #ifdef __cplusplus

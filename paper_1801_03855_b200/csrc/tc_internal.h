@@ -21,13 +21,22 @@ constexpr int kMaxCtas = 1024;                 // per barrier and source rank
 constexpr int kNumBarriers = 3;                // entry, mid, exit
 constexpr size_t kFlagWords = (size_t)kNumBarriers * kMaxRanks * kMaxCtas;
 constexpr size_t kStageCapacity = 8u << 20;    // one-shot staging bytes per parity
+constexpr size_t kLLBytes = 16u << 20;         // low-latency receive buffers (after staging)
+constexpr int64_t kDefaultLLMax = 1 << 20;
 constexpr int64_t kDefaultOneshotMax = 256 << 10;
 constexpr int kPieceShift = 7;                 // work piece = 128 slots = 2 KiB per operand
 constexpr int kPiece = 1 << kPieceShift;
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
-enum Algo { ALGO_LOCAL = 0, ALGO_TWOSHOT = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT_PUSH = 3, ALGO_NVLS = 4 };
+enum Algo {
+  ALGO_LOCAL = 0,
+  ALGO_TWOSHOT = 1,
+  ALGO_ONESHOT = 2,
+  ALGO_TWOSHOT_PUSH = 3,
+  ALGO_NVLS = 4,
+  ALGO_LL = 5
+};
 
 // ---------------------------------------------------------------- A1 descriptor (host)
 struct Plan {
@@ -81,7 +90,8 @@ struct KParams {
   float* const* c;       // [p*T] dw (sgd)
   float* const* mc;      // [T] multicast addresses of the primary group (NVLS), or nullptr
   uint32_t* const* flags;// [p] flag buffers (peer-mapped)
-  float* const* stage;   // [p] one-shot staging buffers (peer-mapped), parity-selected
+  float* const* stage;   // [p] one-shot staging (+ low-latency buffers), peer-mapped
+  int ll_cap;            // low-latency elements per source per parity
   float* const* arena;   // [p] per-rank arena: staging chunk x2 (parity) + p receive scratch
   int chunk_cap;         // slots per arena region (>= the largest owner chunk)
   DevState* state;       // [p] device-side call epochs (this process's ranks are valid)
@@ -140,6 +150,7 @@ struct Comm {
   int variant = 0;                // launch-shape experiment (env TC_VARIANT)
   int tune_ctas = 0, tune_threads = 512;
   int64_t tune_oneshot = -1;
+  int64_t tune_ll = -1;
   unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;
   int absent_rank = -1;
   unsigned long long* prof = nullptr;

@@ -349,6 +349,30 @@ __device__ __forceinline__ void slot_loop(const KParams& kp, int lo, int hi, con
   }
 }
 
+// Small groups: one slot per thread, threads of the grid in order (consecutive threads,
+// consecutive slots), so every slot's tensor lookup runs in parallel instead of a warp walking
+// a piece of many tiny tensors serially.
+template <class Body>
+__device__ __forceinline__ void slot_loop_flat(const KParams& kp, int lo, int hi,
+                                               const Body& body) {
+  TensorCache<Body::NP> tc;
+  tc.t = -1;
+  tc.lo = tc.hi = 0;
+  const int stride = gridDim.x * blockDim.x;
+  for (int s = lo + blockIdx.x * blockDim.x + threadIdx.x; s < hi; s += stride) {
+    SlotRef ref;
+    typename Body::State st;
+    resolve(kp, body, tc, s, ref);
+    if (ref.vec) {
+      body.template load<true>(ref, tc.ptr, st);
+      body.template finish<true>(ref, st);
+    } else {
+      body.template load<false>(ref, tc.ptr, st);
+      body.template finish<false>(ref, st);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ phase bodies
 enum SrcKind {
   SRC_TENSORS = 0,   // every rank's primary tensor (pull reduce-scatter, local path)
@@ -616,6 +640,110 @@ struct NvlsBody {
   }
 };
 
+// ------------------------------------------------------------------ low-latency (LL)
+// Rank r's words for peer k live in k's LL buffer [parity][source r][4*slot + lane]: 8 bytes =
+// {epoch, value bits}.  8-byte stores are single-copy atomic, so a reader that sees the current
+// epoch in a word also sees that word's value -- no separate flag, no barrier.  The parity half
+// a call writes was last read two calls ago, which every peer finished before this call began.
+__device__ __forceinline__ unsigned long long* ll_buf(const KParams& kp, int rank, int par,
+                                                      int src) {
+  return reinterpret_cast<unsigned long long*>(kp.stage[rank] + 2 * (kStageCapacity / sizeof(float))) +
+         ((size_t)par * kp.p + src) * (size_t)kp.ll_cap;
+}
+__device__ __forceinline__ void st_ll(unsigned long long* p, float a, float b, uint32_t e) {
+  const unsigned long long x = ((unsigned long long)e << 32) | __float_as_uint(a);
+  const unsigned long long y = ((unsigned long long)e << 32) | __float_as_uint(b);
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ void ld_ll(const unsigned long long* p, unsigned long long& x,
+                                      unsigned long long& y) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+
+template <int OP, int P>
+struct LLBody {
+  using N = Needs<OP, PH_RS, P>;
+  static constexpr int NP = 3;
+  const KParams& kp;
+  int r;
+  int par;
+  struct State {
+    float4 own, b, c;
+    float *pa, *pb, *pc;
+  };
+  __device__ __forceinline__ void bind(int t, float** ptr) const {
+    const size_t mine = (size_t)r * kp.T + t;
+    ptr[0] = kp.a[mine];
+    ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
+    ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
+  }
+  // Issue the local loads and push this slot to every peer.
+  template <bool VEC>
+  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
+    st.own = ldv<VEC>(ptr[0], ref);
+    if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
+    if constexpr (N::loadC) st.c = ldv<VEC>(ptr[2], ref);
+    st.pa = ptr[0];
+    st.pb = ptr[1];
+    st.pc = ptr[2];
+    const uint32_t e = ep();
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      if (k == r) continue;
+      unsigned long long* dst = ll_buf(kp, k, par, r) + 4 * (size_t)ref.s;
+      st_ll(dst, st.own.x, st.own.y, e);
+      st_ll(dst + 2, st.own.z, st.own.w, e);
+    }
+  }
+  // Wait for every peer's words of this slot, reduce in rank order, apply the epilogue.
+  template <bool VEC>
+  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
+    const uint32_t e = ep();
+    float4 in[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      if (k == r) {
+        in[k] = st.own;
+        continue;
+      }
+      const unsigned long long* src = ll_buf(kp, r, par, k) + 4 * (size_t)ref.s;
+      unsigned long long x0, x1, x2, x3;
+      unsigned long long t0 = 0;
+      while (true) {
+        ld_ll(src, x0, x1);
+        ld_ll(src + 2, x2, x3);
+        if ((uint32_t)(x0 >> 32) == e && (uint32_t)(x1 >> 32) == e && (uint32_t)(x2 >> 32) == e &&
+            (uint32_t)(x3 >> 32) == e)
+          break;
+        if (t0 == 0) t0 = globaltimer();
+        else if (globaltimer() - t0 > kp.timeout_ns) {
+          atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
+          break;
+        }
+      }
+      in[k] = make_float4(__uint_as_float((uint32_t)x0), __uint_as_float((uint32_t)x1),
+                          __uint_as_float((uint32_t)x2), __uint_as_float((uint32_t)x3));
+    }
+    float4 oa;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float v[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) v[k] = lane(in[k], i);
+      float la = 0.f;
+      float lb = N::loadB ? lane(st.b, i) : 0.f;
+      float lc = N::loadC ? lane(st.c, i) : 0.f;
+      elem<OP, PH_RS, P>(kp, r, v, la, lb, lc);
+      lane(oa, i) = la;
+      if constexpr (N::storeB) lane(st.b, i) = lb;
+      if constexpr (N::storeC) lane(st.c, i) = lc;
+    }
+    if constexpr (N::storeA) stv<VEC>(st.pa, ref, oa);
+    if constexpr (N::storeB) stv<VEC>(st.pb, ref, st.b);
+    if constexpr (N::storeC) stv<VEC>(st.pc, ref, st.c);
+  }
+};
+
 // ------------------------------------------------------------------ kernels
 template <int OP, int P, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_twoshot_pull(KParams kp) {
@@ -692,6 +820,19 @@ __global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
   stamp(kp, 5);
 }
 
+// Low-latency: no barrier; each slot is pushed to every peer and its peers' words awaited.
+template <int OP, int P, int MINB>
+__global__ void __launch_bounds__(512, MINB) k_ll(KParams kp) {
+  const int r = kp.rank0 + (int)blockIdx.y;
+  if (r == kp.absent_rank) return;
+  call_begin(kp, r);
+  stamp(kp, 0);
+  LLBody<OP, P> body{kp, r, (int)(ep() & 1u)};
+  slot_loop_flat(kp, 0, kp.M, body);
+  call_end(kp, r);
+  stamp(kp, 5);
+}
+
 // NVLS: ENTRY barrier -> owner slots reduced in the switch and multicast back -> MID barrier
 // (every owner's stores landed everywhere) -> SGD epilogue over this CTA's pieces of every
 // chunk from local memory.  Per GPU: ~(1 + 1/p) S of NVLink traffic each way.
@@ -759,6 +900,8 @@ const void* kernel_ptr(int algo, int p, int variant) {
       if (algo == ALGO_NVLS)                                                         \
         return variant == 1 ? (const void*)k_nvls<OP, PP, 1> : (const void*)k_nvls<OP, PP, 2>; \
     if (algo == ALGO_NVLS) return nullptr;                                           \
+    if (algo == ALGO_LL)                                                             \
+      return variant == 1 ? (const void*)k_ll<OP, PP, 1> : (const void*)k_ll<OP, PP, 2>; \
     if (variant == 1)                                                                \
       return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 1>           \
            : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 1>      \

@@ -67,7 +67,8 @@ unsigned long long env_timeout_ns() {
 tc_status alloc_comm_buffers(Comm& c, int r) {
   TC_CUDA(cudaMalloc((void**)&c.flags[r], kFlagWords * sizeof(uint32_t)));
   TC_CUDA(cudaMemset(c.flags[r], 0, kFlagWords * sizeof(uint32_t)));
-  TC_CUDA(cudaMalloc((void**)&c.stage[r], 2 * kStageCapacity));
+  TC_CUDA(cudaMalloc((void**)&c.stage[r], 2 * kStageCapacity + kLLBytes));
+  TC_CUDA(cudaMemset((char*)c.stage[r] + 2 * kStageCapacity, 0, kLLBytes));
   return TC_OK;
 }
 
@@ -288,6 +289,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.mc = ga->d_mc;
   kp.flags = c.d_flags;
   kp.stage = c.d_stage;
+  kp.ll_cap = (int)(kLLBytes / 2 / 8 / p) & ~(size_t)3;
   kp.arena = c.d_arena;
   kp.chunk_cap = (int)c.arena_cap;
   kp.scale = scale;
@@ -323,7 +325,17 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     // NCCL 70/185/685); p >= 6 -> NVLS when the group is multicast-bound (it moves (1 + 1/p) S
     // per GPU instead of 2(p-1)/p S, 1.56x less at p = 8), else pulled.
     const bool nvls_ok = ga->d_mc != nullptr && op != OP_EASGD;
-    if (bytes <= lim) algo = ALGO_ONESHOT;
+    // Low-latency (LL): every element travels once to every peer as an 8-byte {value, epoch}
+    // word and is awaited in local memory -- no barrier round trip (small groups only).
+    // Measured crossover vs one-shot (config-5 sweep): LL wins up to 1 MiB at p = 2 (12.6 vs
+    // 20.6 us), up to 256 KiB at p = 4 (1 MiB: 29 vs 23 us).  Limits compare the group's data
+    // bytes; the buffers' capacities the padded slot grid.
+    const int64_t data_bytes = pl.N * 4;
+    const int64_t ll_cap = (int64_t)(kLLBytes / 2 / 8 / p) & ~(size_t)3;
+    const int64_t ll_auto = p == 2 ? kDefaultLLMax : (p <= 4 ? kDefaultLLMax / 2 : kDefaultLLMax / 8);
+    const int64_t ll_lim = c.tune_ll < 0 ? ll_auto : c.tune_ll;
+    if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
+    else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;
     else if (c.algo_override == ALGO_TWOSHOT_PUSH) algo = ALGO_TWOSHOT_PUSH;
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
     else if (nvls_ok && (c.algo_override == ALGO_NVLS || p >= 6)) algo = ALGO_NVLS;
@@ -345,7 +357,8 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   } else if (twoshot && c.tune_ctas > 0) {
     ctas = c.tune_ctas;
   } else {
-    ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * (algo == ALGO_ONESHOT ? 1 : occ));
+    ctas = (int)std::min<int64_t>(
+        want, (int64_t)c.num_sms * ((algo == ALGO_ONESHOT || algo == ALGO_LL) ? 1 : occ));
   }
   if (algo != ALGO_LOCAL) {
     if (ctas > kMaxCtas) ctas = kMaxCtas;
@@ -487,6 +500,12 @@ tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t o
   comm->c.tune_ctas = num_ctas;
   comm->c.tune_threads = threads ? threads : 512;
   comm->c.tune_oneshot = oneshot_max;
+  return TC_OK;
+}
+
+tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes) {
+  if (!comm || bytes < -1) return TC_ERR_INVALID_ARG;
+  comm->c.tune_ll = bytes;
   return TC_OK;
 }
 

@@ -27,7 +27,7 @@ STATUS = {
 }
 TC_OK, TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_NOT_SHAREABLE = 0, 1, 2, 3
 TC_ERR_BUSY, TC_ERR_TIMEOUT, TC_ERR_CUDA, TC_ERR_BOOTSTRAP, TC_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
-ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 3: "two-shot-push", 4: "nvls"}
+ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 3: "two-shot-push", 4: "nvls", 5: "ll"}
 ALGO_AUTO, ALGO_TWOSHOT_PULL, ALGO_TWOSHOT_PUSH, ALGO_NVLS = 0, 1, 3, 4
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -56,6 +56,7 @@ _SIGS = {
     "tc_comm_set_tuning": (_c_int, [_vp, _c_int, _c_int, _c_int64]),
     "tc_comm_set_timeout": (_c_int, [_vp, _c_int64]),
     "tc_comm_set_algorithm": (_c_int, [_vp, _c_int]),
+    "tc_comm_set_ll_max": (_c_int, [_vp, _c_int64]),
     "tc_mem_alloc": (_c_int, [_vp, ctypes.c_size_t, _pp]),
     "tc_mem_free": (_c_int, [_vp, _vp]),
     "tc_comm_multicast_supported": (_c_int, [_vp]),
@@ -264,6 +265,10 @@ class Comm:
         """0 = automatic, 1 = two-shot pull, 3 = two-shot push (identical results),
         4 = NVLS for groups in symmetric memory."""
         _check(LIB.tc_comm_set_algorithm(self.h, int(algo)), "set_algorithm")
+
+    def set_ll_max(self, nbytes: int):
+        """Groups up to nbytes use the low-latency algorithm (-1 automatic, 0 never)."""
+        _check(LIB.tc_comm_set_ll_max(self.h, int(nbytes)), "set_ll_max")
 
     def set_timeout(self, ms: int):
         _check(LIB.tc_comm_set_timeout(self.h, int(ms)), "set_timeout")

@@ -32,9 +32,10 @@ def main():
     cases = [(W.TINY, "int", 0), (W.TINY, "int", 1 << 20),
              ([7, 13, 1000, 0, 50001, 3, 262144], "grad", 0),
              ([7, 13, 1000, 0, 5001, 3], "grad", 1 << 20)]
-    for (numels, kind, oneshot), algo in [(c, a) for c in cases for a in (1, 3)]:
+    for (numels, kind, oneshot), algo in [(c, a) for c in cases for a in (1, 3, 5)]:
         comm.set_tuning(0, 0, oneshot)
-        comm.set_algorithm(algo)
+        comm.set_ll_max(1 << 30 if algo == 5 else 0)
+        comm.set_algorithm(algo if algo != 5 else 0)
         xs = [W.group(numels, kind, 60, 0, k, W.GRAD) for k in range(p)]
         dev = to_dev(xs[rank])
         with tc.Group(comm, dev) as g:
@@ -43,9 +44,10 @@ def main():
         assert comm.async_error() == 0
 
     # SGD (fused) and EASGD, two-shot and one-shot
-    for oneshot, algo in ((0, 1), (0, 3), (1 << 20, 0)):
+    for oneshot, algo in ((0, 1), (0, 3), (1 << 20, 0), (0, 5)):
         comm.set_tuning(0, 0, oneshot)
-        comm.set_algorithm(algo)
+        comm.set_ll_max(1 << 30 if algo == 5 else 0)
+        comm.set_algorithm(algo if algo != 5 else 0)
         numels = [7, 13, 1000, 4096, 65]
         gs = [W.group(numels, "grad", 61, 0, k, W.GRAD) for k in range(p)]
         w = W.group(numels, "param", 61, 0, 0, W.PARAM)
@@ -75,6 +77,7 @@ def main():
     views = list(torch.split(sym[:sum(numels)], numels))
     algos = [1, 3] + ([4] if comm.multicast_supported else [])
     comm.set_tuning(0, 0, 0)
+    comm.set_ll_max(0)
     with tc.Group(comm, views) as g:
         for algo in algos:
             comm.set_algorithm(algo)
@@ -128,6 +131,7 @@ def main():
 
     # full-size ResNet-50 gradient group, fused SGD, checked on a sample of elements
     comm.set_tuning(0, 0, -1)
+    comm.set_ll_max(-1)
     comm.set_algorithm(3 if p % 2 == 0 else 1)
     numels = W.RESNET50
     gs = [W.group(numels, "grad", W.CFG_RESNET50, 0, k, W.GRAD) for k in range(p)]

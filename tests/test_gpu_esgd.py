@@ -21,7 +21,7 @@ from gpu_util import to_dev, to_host, assert_bitwise  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kind,oneshot", [("grad", 0), ("grad", 1 << 20), ("int", 0)])
+@pytest.mark.parametrize("kind,oneshot", [("grad", 0), ("grad", 1 << 20), ("int", 0), ("grad", "ll")])
 def test_config4_esgd_sequence(kind, oneshot):
     numels = [7, 13, 1000, 4096, 65]
     C, Q, steps, tau = 2, 4, 16, 4          # clients, GPUs per client
@@ -46,7 +46,11 @@ def test_config4_esgd_sequence(kind, oneshot):
     clients = [tc.Comm.emulated(Q, 0) for _ in range(C)]
     pairs = [tc.Comm.emulated(C, 0) for _ in range(Q)]
     for cm in clients + pairs:
-        cm.set_tuning(0, 0, oneshot)
+        if oneshot == "ll":
+            cm.set_ll_max(1 << 30)
+        else:
+            cm.set_ll_max(0)
+            cm.set_tuning(0, 0, oneshot)
     G = [tc.Group(clients[i], [g[Q * i + k] for k in range(Q)]) for i in range(C)]
     Wt = [tc.Group(clients[i], [x[Q * i + k] for k in range(Q)]) for i in range(C)]
     D = [tc.Group(clients[i], [dw[Q * i + k] for k in range(Q)]) for i in range(C)]

@@ -15,13 +15,14 @@ from gpu_util import to_dev, to_host, assert_bitwise  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("oneshot", [0, 1 << 20])
-def test_graph_capture_and_replay(oneshot):
+@pytest.mark.parametrize("oneshot,ll", [(0, 0), (1 << 20, 0), (0, 1 << 20)])
+def test_graph_capture_and_replay(oneshot, ll):
     p = 4
     numels = [7, 13, 1000, 4096]
     xs = [W.group(numels, "int", 55, 0, k, W.GRAD) for k in range(p)]
     comm = tc.Comm.emulated(p, 0)
     comm.set_tuning(0, 0, oneshot)
+    comm.set_ll_max(ll)
     dev = [to_dev(x) for x in xs]
     grp = tc.Group(comm, dev)
     pristine = [[t.clone() for t in d] for d in dev]

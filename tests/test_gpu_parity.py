@@ -26,11 +26,17 @@ pytestmark = pytest.mark.gpu
 ONESHOT = 1 << 20   # force one-shot
 TWOSHOT = 0         # force two-shot (pull reduce-scatter)
 PUSH = -2           # force two-shot with pushed reduce-scatter
-ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT)]
+LL = -3             # force the low-latency algorithm
+ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT), ("ll", LL)]
 
 
 def _comm(p, oneshot=-1, ctas=0):
     c = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
+    if oneshot == LL:
+        c.set_ll_max(1 << 30)
+        return c
+    if oneshot != -1:
+        c.set_ll_max(0)
     if oneshot == PUSH:
         c.set_algorithm(3)
         oneshot = 0
@@ -96,7 +102,7 @@ def test_unaligned_tensors(p, offset):
     numels = [7, 13, 1000, 4096, 3, 1, 2]
     xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
     off = (lambda k: k % 4) if offset == "per-rank" else offset
-    for oneshot in (TWOSHOT, PUSH, ONESHOT):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL):
         out, _ = run_allreduce(xs, oneshot=oneshot, offset=off)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -144,7 +150,7 @@ def test_many_tensors_1024():
     g = np.random.default_rng(5)
     numels = W.random_numels(g, 1024, 700)
     xs = [W.group(numels, "grad", 74, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, ONESHOT):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -182,6 +188,7 @@ def test_repeated_calls_epochs():
     for i in range(40):
         comm.set_algorithm(3 if i % 2 else 1)
         comm.set_tuning(0, 0, ONESHOT if i % 3 == 0 else TWOSHOT)
+        comm.set_ll_max(1 << 30 if i % 5 == 0 else 0)
         tc.allreduce(grp, 1.0 / p if i == 0 else 1.0 / p)
         if i == 0:
             first = [to_host(d) for d in dev]
@@ -377,7 +384,9 @@ def test_config5_sweep_shapes(p, T):
         if not numels:
             continue
         xs = [W.group(numels, "grad", W.CFG_SWEEP, 0, k, W.GRAD) for k in range(p)]
-        for oneshot in (TWOSHOT, ONESHOT):
+        for oneshot in (TWOSHOT, ONESHOT, LL):
+            if oneshot == LL and total > (64 << 10):
+                continue
             comm = _comm(p, oneshot)
             flats = [torch.from_numpy(np.concatenate(x)).cuda() for x in xs]
             views = [list(torch.split(f, numels)) for f in flats]

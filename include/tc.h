@@ -140,8 +140,8 @@ TC_API tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes);
  * multimem.st; only for groups in tc_mem_alloc memory, else two-shot).  1 and 3 end with the
  * staged pull allgather and give bit-identical results (float64, rank order).  NVLS sums in
  * the switch in fp32 (order unspecified): exact for integer-valued data, else within
- * (p-1) ulp-scale of the float64 sum; identical on every rank.  Automatic: pull up to
- * p = 5, p >= 6 NVLS for eligible groups (else pull).  Errors: TC_ERR_INVALID_ARG. */
+ * (p-1) ulp-scale of the float64 sum; identical on every rank.  Automatic: pull, except
+ * tc_allreduce of eligible groups at p >= 6 -> NVLS.  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 
 /* Device-barrier timeout in milliseconds (default 30000, or env TC_TIMEOUT_MS). */

@@ -1,0 +1,138 @@
+#!/usr/bin/env python
+"""NEXT row f1: the fused SGD step overlapped with a (synthetic) backward pass, bucket by bucket.
+
+    torchrun --nproc-per-node N bench_overlap.py [--ratio 1.0] [--bucket-mb 25]
+
+PAPER.md:59: gradients "are obtained as soon as a backward step for a layer is computed, these
+can be aggregated in parallel with the backward phase".  The backward pass is synthetic: for each
+ResNet-50 tensor, last to first, a bf16 GEMM burst sized so the whole pass takes `ratio` x the
+time of one whole-group tc_sgd_step, then the tensor's gradient is written.  Three runs:
+  compute  -- the backward pass alone;
+  serial   -- backward, then one tc_sgd_step over the whole group;
+  overlap  -- tc.BucketedStep: each bucket's tc_sgd_step on a side stream once its last gradient
+              is written, with the collective kernels limited to `ctas` CTAs so the GEMMs keep
+              SMs (several budgets).
+Rank 0 prints one JSON line per configuration with the fraction of the step hidden.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+import paper_1801_03855_b200 as tc  # noqa: E402
+import tc_workloads as W  # noqa: E402
+
+
+def timed(fn, iters, world):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / iters], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t) * 1e3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ratio", type=float, default=1.0)
+    ap.add_argument("--bucket-mb", type=float, default=25.0)
+    ap.add_argument("--iters", type=int, default=10)
+    a = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    numels = W.RESNET50
+    N = sum(numels)
+
+    def flat(kind, role):
+        f = torch.from_numpy(np.concatenate(W.group(numels, kind, W.CFG_RESNET50, 0, rank, role)))
+        f = f.cuda()
+        return f, list(torch.split(f, numels))
+
+    gp_flat, gp = flat("grad", W.GRAD)
+    g_flat, g = flat("grad", W.GRAD)
+    w_flat, w = flat("param", W.PARAM)
+    d_flat, dw = flat("dw", W.DW)
+    comm = tc.Comm.single(local) if world == 1 else tc.Comm.from_process_group(device=local)
+    hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (world * 128))
+    G, Wg, D = tc.Group(comm, g), tc.Group(comm, w), tc.Group(comm, dw)
+
+    def whole_step():
+        tc.sgd_step(Wg, G, D, **hp)
+
+    comm.set_tuning(0, 0, -1)
+    t_step = timed(lambda: (g_flat.copy_(gp_flat), whole_step()), a.iters, world) - \
+        timed(lambda: g_flat.copy_(gp_flat), a.iters, world)
+    A = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
+    C = torch.empty_like(A)
+    t_gemm = timed(lambda: torch.mm(A, B, out=C), 50, world)
+    total_gemms = max(1, int(round(a.ratio * t_step / t_gemm)))
+    # The synthetic backward works bucket by bucket (few launches, so the host is not the
+    # bottleneck): a GEMM burst proportional to the bucket's bytes, then one copy writing the
+    # bucket's gradients (contiguous views of the flat gradient buffer), last layers first.
+    bucket_of, nb = tc.Plan(numels).buckets(int(a.bucket_mb * (1 << 20)))
+    members = [[t for t in range(len(numels)) if bucket_of[t] == k] for k in range(nb)]
+    offs = np.concatenate([[0], np.cumsum(numels)])
+    spans = [(int(offs[m[0]]), int(offs[m[-1] + 1])) for m in members]
+    per = [max(1, int(round(total_gemms * (hi - lo) / N))) for lo, hi in spans]
+
+    def backward(after=None):
+        for k in range(nb):
+            for _ in range(per[k]):
+                torch.mm(A, B, out=C)
+            lo, hi = spans[k]
+            g_flat[lo:hi].copy_(gp_flat[lo:hi])
+            if after:
+                for t in reversed(members[k]):
+                    after(t)
+
+    t_compute = timed(backward, a.iters, world)
+    t_serial = timed(lambda: (backward(), whole_step()), a.iters, world)
+    rows = []
+    for ctas in (0, 148, 64, 32):
+        step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas)
+
+        def overlapped():
+            backward(lambda t: step.grad_ready(t, **hp))
+            step.finish()
+
+        t_over = timed(overlapped, a.iters, world)
+        comm.set_tuning(0, 0, -1)
+        rows.append({"bench": "overlap (NEXT row f1)", "n_gpus": world, "ctas": ctas or "auto",
+                     "buckets": step.nbuckets, "bucket_mb": a.bucket_mb,
+                     "ratio": a.ratio, "gemms": sum(per),
+                     "t_step_us": t_step, "t_compute_us": t_compute, "t_serial_us": t_serial,
+                     "t_overlap_us": t_over,
+                     "hidden_fraction": (t_serial - t_over) / max(t_serial - t_compute, 1e-9),
+                     "speedup_vs_serial": t_serial / t_over})
+        step.destroy()
+    if rank == 0:
+        for r in rows:
+            print(json.dumps(r), flush=True)
+    for grp in (G, Wg, D):
+        grp.destroy()
+    comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

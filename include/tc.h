@@ -101,6 +101,15 @@ TC_API int tc_plan_num_segments(const tc_plan* plan);
 TC_API tc_status tc_plan_segment(const tc_plan* plan, int i, int* tensor, int* owner,
                           int64_t* slot_lo, int64_t* slot_hi);
 
+/* NEXT row f1 -- bucketed reduction overlapped with the backward pass (gradients "can be
+ * aggregated in parallel with the backward phase").  Assigns every tensor a bucket: tensors are
+ * taken from the last to the first (backward order) and grouped while a bucket holds at most
+ * `bucket_bytes` (a larger tensor is a bucket of its own).  Writes bucket_of_tensor[T] (bucket 0
+ * = first ready) and returns the number of buckets, or -1 on a bad argument.  Each bucket is
+ * then an ordinary tc_group whose reduction (tc_allreduce / tc_sgd_step) is launched on a side
+ * stream as soon as its last gradient is produced. */
+TC_API int tc_plan_buckets(const tc_plan* plan, int64_t bucket_bytes, int* bucket_of_tensor);
+
 /* ---------------------------------------------------------------------------------------
  * Communicators.
  * --------------------------------------------------------------------------------------- */

@@ -6,4 +6,5 @@ raises if it has not been built -- there is no CPU fallback.
 """
 from .tc import (  # noqa: F401
     Comm, Group, Plan, TcError, allreduce, sgd_step, easgd_update, LIB, LIB_PATH, STATUS,
+    BucketedStep,
 )

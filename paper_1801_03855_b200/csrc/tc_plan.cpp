@@ -140,4 +140,28 @@ tc_status tc_plan_segment(const tc_plan* plan, int i, int* tensor, int* owner, i
   return TC_OK;
 }
 
+int tc_plan_buckets(const tc_plan* plan, int64_t bucket_bytes, int* bucket_of_tensor) {
+  // NEXT row f1 (gradients "can be aggregated in parallel with the backward phase"):
+  // consecutive tensors, taken from the last to the first -- the order a backward pass produces
+  // them -- are grouped while the bucket stays within bucket_bytes; a larger tensor is a bucket
+  // of its own.  Bucket 0 is the first ready (it holds the last tensors).
+  if (!plan || !bucket_of_tensor || bucket_bytes <= 0) return -1;
+  const Plan& p = plan->p;
+  int b = 0;
+  int64_t fill = 0;
+  bool open = false;
+  for (int t = p.T - 1; t >= 0; --t) {
+    const int64_t bytes = p.numel[(size_t)t] * 4;
+    if (open && fill + bytes > bucket_bytes) {
+      ++b;
+      fill = 0;
+      open = false;
+    }
+    bucket_of_tensor[t] = b;
+    fill += bytes;
+    open = true;
+  }
+  return open ? b + 1 : b;
+}
+
 }  // extern "C"

@@ -41,6 +41,7 @@ _SIGS = {
     "tc_plan_create": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_int64), ALLGATHER_FN,
                                 _vp, _pp]),
     "tc_plan_destroy": (None, [_vp]),
+    "tc_plan_buckets": (_c_int, [_vp, _c_int64, ctypes.POINTER(_c_int)]),
     "tc_plan_num_elements": (_c_int64, [_vp]),
     "tc_plan_num_slots": (_c_int64, [_vp]),
     "tc_plan_hash": (ctypes.c_uint64, [_vp]),
@@ -141,6 +142,7 @@ class Plan:
         _check(LIB.tc_plan_create(rank, nranks, len(numels), arr, self._ag, None, ctypes.byref(h)),
                "tc_plan_create")
         self.h = h
+        self.num_tensors = len(numels)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -168,6 +170,14 @@ class Plan:
         a, b = ctypes.c_int64(), ctypes.c_int64()
         _check(LIB.tc_plan_owner_range(self.h, r, ctypes.byref(a), ctypes.byref(b)), "owner_range")
         return a.value, b.value
+
+    def buckets(self, bucket_bytes: int):
+        """Bucket index of every tensor (backward order, bucket 0 first ready)."""
+        out = (ctypes.c_int * self.num_tensors)()
+        n = LIB.tc_plan_buckets(self.h, int(bucket_bytes), out)
+        if n < 0:
+            raise TcError(TC_ERR_INVALID_ARG, "tc_plan_buckets")
+        return list(out), n
 
     def segments(self):
         out = []
@@ -372,3 +382,70 @@ def sgd_step(w: Group, g: Group, dw: Group, lr: float, momentum: float = 0.0, wd
 def easgd_update(x: Group, center: Group, alpha: float, stream=None):
     _check(LIB.tc_easgd_update(x.h, center.h, float(alpha), _stream_ptr(stream)),
            "tc_easgd_update")
+
+
+class BucketedStep:
+    """Bucketed, overlapped fused step (NEXT row f1).
+
+    The gradient group is split into buckets (tc_plan_buckets, backward order).  After the
+    backward pass has produced every gradient of a bucket (``grad_ready(t)`` for each of its
+    tensors, called on the compute stream in production order), the bucket's tc_sgd_step -- or
+    tc_allreduce when w/dw are None -- is enqueued on a side stream behind an event, so the
+    reduction and update of early buckets overlap the backward computation of later layers.
+    ``finish()`` makes the compute stream wait for all buckets.  All ranks must produce the
+    gradients in the same order (the bucket calls are collective).
+    """
+
+    def __init__(self, comm, g, w=None, dw=None, bucket_bytes=25 << 20, stream=None, ctas=0):
+        import torch
+        numels = [t.numel() for t in (g[0] if comm.is_emulated else g)]
+        plan = Plan(numels)
+        self.bucket_of, self.nbuckets = plan.buckets(bucket_bytes)
+        self.comm = comm
+        self.stream = stream or torch.cuda.Stream()
+        members = [[] for _ in range(self.nbuckets)]
+        for t in range(len(numels)):
+            members[self.bucket_of[t]].append(t)
+        self.members = members
+
+        def pick(ts, idx):
+            return [[x[i] for i in idx] for x in ts] if comm.is_emulated else [ts[i] for i in idx]
+
+        self.G = [Group(comm, pick(g, m)) for m in members]
+        self.W = [Group(comm, pick(w, m)) for m in members] if w is not None else None
+        self.D = [Group(comm, pick(dw, m)) for m in members] if dw is not None else None
+        self.ctas = ctas
+        self.reset()
+
+    def reset(self):
+        self.missing = [len(m) for m in self.members]
+
+    def grad_ready(self, t, compute_stream=None, **hp):
+        """Tensor t's gradient has been written (on compute_stream).  Launches its bucket's
+        collective when it was the bucket's last tensor."""
+        import torch
+        b = self.bucket_of[t]
+        self.missing[b] -= 1
+        if self.missing[b]:
+            return
+        ev = torch.cuda.Event()
+        ev.record(compute_stream or torch.cuda.current_stream())
+        self.stream.wait_event(ev)
+        if self.ctas:
+            self.comm.set_tuning(self.ctas, 0, -1)
+        if self.W is not None:
+            sgd_step(self.W[b], self.G[b], self.D[b], stream=self.stream, **hp)
+        else:
+            allreduce(self.G[b], hp.get("scale", 1.0), stream=self.stream)
+
+    def finish(self, compute_stream=None):
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        (compute_stream or torch.cuda.current_stream()).wait_event(ev)
+        self.reset()
+
+    def destroy(self):
+        for gs in (self.G, self.W or [], self.D or []):
+            for grp in gs:
+                grp.destroy()

@@ -91,3 +91,21 @@ def test_hot_path_rejects_null_handles_without_a_gpu():
     assert LIB.tc_sgd_step(None, None, None, 0.1, 0.9, 0.0, 1.0, None) == tc.tc.TC_ERR_INVALID_ARG
     assert LIB.tc_easgd_update(None, None, 0.1, None) == tc.tc.TC_ERR_INVALID_ARG
     assert LIB.tc_comm_async_error(None) == tc.tc.TC_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("cap", [1 << 10, 1 << 20, 25 << 20, 1 << 40])
+def test_buckets_backward_order(cap):
+    """NEXT row f1: buckets are runs of consecutive tensors in backward order, within the byte cap
+    unless a single tensor exceeds it, covering every tensor once."""
+    numels = W.RESNET50
+    b, n = tc.Plan(numels).buckets(cap)
+    assert n >= 1 and sorted(set(b)) == list(range(n))
+    assert b[-1] == 0 and b == sorted(b, reverse=True)      # backward order, bucket 0 first
+    for k in range(n):
+        members = [t for t in range(len(numels)) if b[t] == k]
+        assert members == list(range(members[0], members[-1] + 1))
+        size = 4 * sum(numels[t] for t in members)
+        assert size <= cap or len(members) == 1
+        if k + 1 < n:  # greedy: the next tensor would not have fitted
+            nxt = members[0] - 1
+            assert size + 4 * numels[nxt] > cap

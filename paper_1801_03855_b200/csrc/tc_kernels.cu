@@ -555,19 +555,18 @@ __device__ bool wait_one(const KParams& kp, int r, int q, int bar) {
   return ok != 0;
 }
 
-// Staged allgather: publish my staged chunk, then pull every other owner's chunk once that
-// owner's CTA has staged it, owners r+1, r+2, ... in turn.  At each step the ranks read from a
-// permutation of the owners, the NVLink pattern B200 serves fastest (p = 4: 117 us per phase;
-// owners mixed per CTA: 134-154 us; "whichever owner is ready first": 155-182 us, the early
-// owners' egress saturates).
+// Staged allgather: once every peer's CTA has staged its chunk (one barrier, so all CTAs start
+// together), pull the other owners' chunks r+1, r+2, ... in turn.  At each step the ranks read
+// from a permutation of the owners, the NVLink pattern B200 serves fastest.  Measured at p = 4
+// (ResNet-50): barrier + rank rotation 117 us; per-owner waits (CTAs drift apart and the steps
+// mix) 131-156 us; owners mixed per CTA 134-154 us; "whichever owner is ready first" 155-182 us.
 template <int OP, int P, int MINB>
 __device__ __forceinline__ bool gather_all(const KParams& kp, int r, int par) {
   const int64_t M = kp.M;
-  signal_all(kp, r, BAR_MID);
+  if (!barrier_all(kp, r, BAR_MID, true)) return false;
 #pragma unroll 1
   for (int j = 0; j < P - 1; ++j) {
     const int q = (r + 1 + j) % P;
-    if (!wait_one(kp, r, q, BAR_MID)) return false;
     const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
     GatherBody<OP> body{kp, r, lo, arena_stage(kp, q, par)};
     slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);

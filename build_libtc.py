@@ -10,14 +10,17 @@ machine without a GPU driver.
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 HERE = os.path.join(ROOT, "paper_1801_03855_b200")
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtc.so")
-SOURCES = ["tc_plan.cpp", "tc_runtime.cu", "tc_symmem.cu", "tc_kernels.cu"]
+SOURCES = ["tc_plan.cpp", "tc_runtime.cu", "tc_symmem.cu", "tc_kernels.cu",
+           "tc_kernels_allreduce.cu", "tc_kernels_sgd.cu", "tc_kernels_easgd.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -34,28 +37,57 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + ["tc_internal.h"]]
+    deps = [os.path.join(CSRC, s) for s in SOURCES + ["tc_internal.h", "tc_kernels.cuh"]]
     deps.append(os.path.join(ROOT, "include", "tc.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if ptxas_info else []) + \
-        [os.path.join(CSRC, s) for s in SOURCES] + ["-o", LIB + ".tmp"]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if verbose or r.returncode != 0:
-        sys.stdout.write(r.stdout)
-        sys.stderr.write(r.stderr)
+def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False,
+          out: str = LIB, defines: tuple = ()) -> str:
+    """Compiles the sources in parallel (one nvcc per file) and links them.  `out`/`defines`
+    build experimental variants (e.g. -DTC_LD_MODE=1) next to the product library."""
+    if not force and out == LIB and not _stale():
+        return out
+    tmp = tempfile.mkdtemp(prefix="libtc_")
+    extra = (["-Xptxas", "-v"] if ptxas_info else []) + [f"-D{d}" for d in defines]
+    objs, procs = [], []
+    for s in SOURCES:
+        obj = os.path.join(tmp, s + ".o")
+        cmd = [NVCC] + FLAGS + extra + ["-c", os.path.join(CSRC, s), "-o", obj]
+        cmd.remove("-shared")
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                          text=True)))
+        objs.append(obj)
+    failed = False
+    for s, pr in procs:
+        so, se = pr.communicate()
+        if verbose or pr.returncode != 0:
+            sys.stdout.write(so)
+            sys.stderr.write(se)
+        failed |= pr.returncode != 0
+    if failed:
+        shutil.rmtree(tmp, ignore_errors=True)
+        raise RuntimeError("nvcc failed")
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+            "-Xcompiler", "-fPIC,-fvisibility=hidden"] + objs + ["-o", out + ".tmp"]
+    r = subprocess.run(link, capture_output=True, text=True)
+    shutil.rmtree(tmp, ignore_errors=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({r.returncode})")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc link failed ({r.returncode})")
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force=True, ptxas_info="-v" in sys.argv)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=LIB)
+    ap.add_argument("-D", action="append", default=[], dest="defines")
+    a = ap.parse_args()
+    build(verbose=a.v, force=True, ptxas_info=a.v, out=os.path.abspath(a.out),
+          defines=tuple(a.defines))

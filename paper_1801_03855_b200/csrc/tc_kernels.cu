@@ -1,1008 +1,18 @@
-// Hot-path kernels of libtc for sm_100a (B200): the tensor allreduce of PAPER.md §6
-// (reduce-scatter + allgather), fused with the SGD step (Eq. 1) or the elastic
-// averaging update (Eqs. elastic1/elastic2).
-//
-// Design:
-//  * One kernel per call.  Each rank runs B CTAs; CTA b of every rank owns the same pieces
-//    of every owner chunk, so cross-GPU synchronisation is per-CTA-pair flag exchange (no grid
-//    sync): the epoch is stored into the peer's flag word [barrier][my rank][b] with
-//    st.release.sys and awaited on the local word with ld.acquire.sys (timeout -> sticky error).
-//  * Every range is cut into 128-slot pieces dealt round-robin to CTAs, then warps: the GPU
-//    streams one contiguous window at a time (DRAM locality) and ranges holding many tiny
-//    tensors (ResNet-50's BN vectors) are spread over all warps.  Each lane resolves its slot's
-//    tensor from a per-128-slot-block tensor table and caches the tensor's pointers.
-//  * Two-shot, pull (A2-A4): ENTRY barrier -> reduce-scatter: each owned slot pulls the 16-B
-//    vectors of all p ranks over NVLink, sums them in float64 in rank order 0..p-1, rounds once,
-//    applies the epilogue, writes in place and into a parity-selected staging chunk -> MID
-//    barrier -> allgather: pull every other owner's staged chunk (rotated start), epilogue.
-//    No exit barrier: peers read only staging, which is rewritten two calls later, after the
-//    next call's first barrier proved every peer finished this one.
-//  * Two-shot, push: every rank first STORES its contribution to each owner's receive scratch
-//    (stores beat loads over NVLink), signalling per owner; the owner reduces from local HBM in
-//    the same canonical order, then the staged pull allgather as above.  No entry barrier.
-//  * One-shot (A5, small groups): copy the group into a parity-selected staging buffer, ENTRY
-//    barrier, every rank reduces all slots from all p staging buffers.
-//  * Local (p = 1): the epilogue as a single HBM stream.
-//  * Arithmetic: float64 accumulation in canonical rank order (R3/R4) and explicit _rn fp32
-//    ops for the SGD/elastic epilogues (no FMA contraction, R5): GPU == CPU oracle bit for bit.
-#include <cuda_runtime.h>
-#include <cstdint>
-
+// Kernel selection and launch (the kernels themselves: tc_kernels.cuh, instantiated per op in
+// tc_kernels_{allreduce,sgd,easgd}.cu).
 #include "tc_internal.h"
 
 namespace tc {
+const void* kernel_ptr_allreduce(int algo, int p, int variant);
+const void* kernel_ptr_sgd(int algo, int p, int variant);
+const void* kernel_ptr_easgd(int algo, int p, int variant);
+
 namespace {
-
-// ------------------------------------------------------------------ memory primitives
-__device__ __forceinline__ float4 ld16(const float* p) {
-  float4 v;
-  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st16(float* p, float4 v) {
-  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ float ld4(const float* p) {
-  float v;
-  asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st4(float* p, float v) {
-  asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ float& lane(float4& v, int i) { return (&v.x)[i]; }
-__device__ __forceinline__ float lane_of(const float4& v, int i) { return (&v.x)[i]; }
-
-// Phase timestamp (diagnostics only; kp.prof == nullptr in production).
-__device__ __forceinline__ void stamp(const KParams& kp, int i) {
-  if (kp.prof != nullptr && threadIdx.x == 0)
-    kp.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = globaltimer();
-}
-
-// ------------------------------------------------------------------ call epoch (device side)
-// Every collective call on a comm gets the next epoch: the kernel reads its rank's counter at
-// start and the last CTA to finish advances it, so no host state enters the kernel arguments and
-// calls can be captured in a CUDA graph and replayed.  Flags compare against the epoch.
-__shared__ uint32_t s_epoch;
-
-__device__ __forceinline__ uint32_t ep() { return s_epoch; }
-// one-shot staging half used by this call (floats)
-__device__ __forceinline__ size_t stage_off() {
-  return (size_t)(s_epoch & 1u) * (kStageCapacity / sizeof(float));
-}
-
-__device__ __forceinline__ void call_begin(const KParams& kp, int r) {
-  if (threadIdx.x == 0) s_epoch = *(volatile uint32_t*)&kp.state[r].epoch + 1u;
-  __syncthreads();
-}
-
-__device__ __forceinline__ void call_end(const KParams& kp, int r) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    DevState* st = kp.state + r;
-    if (atomicAdd(&st->done, 1u) == gridDim.x - 1) {
-      st->done = 0;
-      __threadfence();
-      *(volatile uint32_t*)&st->epoch = s_epoch;
-    }
-  }
-}
-
-// ------------------------------------------------------------------ flags (A2)
-__device__ __forceinline__ size_t flag_index(int bar, int src, int cta) {
-  return ((size_t)bar * kMaxRanks + src) * kMaxCtas + cta;
-}
-
-// Thread 0: tell rank `to` that this CTA (rank r) passed point `bar`.  Caller has synced.
-__device__ __forceinline__ void signal_one(const KParams& kp, int bar, int r, int to) {
-  st_release_sys(kp.flags[to] + flag_index(bar, r, blockIdx.x), ep());
-}
-
-// Whole CTA: publish arrival at `bar` to every peer (if do_signal), then wait for every
-// peer's arrival.  Returns false (CTA must stop) on timeout.
-__device__ bool barrier_all(const KParams& kp, int r, int bar, bool do_signal) {
-  __syncthreads();  // every thread's prior stores of this CTA precede the release below
-  const int k = threadIdx.x;
-  bool ok = true;
-  if (k < kp.p && k != r) {
-    if (do_signal) st_release_sys(kp.flags[k] + flag_index(bar, r, blockIdx.x), ep());
-    const uint32_t* mine = kp.flags[r] + flag_index(bar, k, blockIdx.x);
-    if ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
-      const unsigned long long t0 = globaltimer();
-      while ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
-        if (globaltimer() - t0 > kp.timeout_ns) {
-          atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
-          ok = false;
-          break;
-        }
-      }
-    }
-  }
-  return __syncthreads_and(ok) != 0;
-}
-
-// Whole CTA: publish arrival at `bar` to every peer without waiting.
-__device__ __forceinline__ void signal_all(const KParams& kp, int r, int bar) {
-  __syncthreads();
-  const int k = threadIdx.x;
-  if (k < kp.p && k != r) st_release_sys(kp.flags[k] + flag_index(bar, r, blockIdx.x), ep());
-}
-
-// ------------------------------------------------------------------ element arithmetic
-enum Phase { PH_RS = 0, PH_AG = 1 };
-
-// Local operands of (op, phase): A = primary (x / g), B = w or center, C = dw.
-template <int OP, int PH, int P> struct Needs {
-  static constexpr bool loadA = (OP == OP_EASGD && PH == PH_AG);
-  static constexpr bool loadB = (OP == OP_SGD) || (OP == OP_EASGD);
-  static constexpr bool loadC = (OP == OP_SGD);
-  // p = 1 SGD: the reduced gradient is the gradient itself -- not stored back.
-  static constexpr bool storeA = !(OP == OP_SGD && PH == PH_RS && P == 1);
-  static constexpr bool storeB = (OP == OP_SGD) || (OP == OP_EASGD);
-  static constexpr bool storeC = (OP == OP_SGD);
-};
-
-// SGD epilogue (A6), fp32 mirror of the oracle: t = R(R(rs*G)+R(wd*w)); dw' = R(R(mu*dw)-R(lr*t));
-// w' = R(w+dw').
-__device__ __forceinline__ void sgd1(const KParams& kp, float G, float& w, float& dw) {
-  const float t = __fadd_rn(__fmul_rn(kp.rescale, G), __fmul_rn(kp.wd, w));
-  dw = __fsub_rn(__fmul_rn(kp.mu, dw), __fmul_rn(kp.lr, t));
-  w = __fadd_rn(w, dw);
-}
-
-// One element.  in[k]: P source values (PH_RS) or the owner's value in[0] (PH_AG).
-// la/lb/lc: local operands in, results out.
-template <int OP, int PH, int P>
-__device__ __forceinline__ void elem(const KParams& kp, int r, const float* in, float& la,
-                                     float& lb, float& lc) {
-  if constexpr (OP == OP_ALLREDUCE) {
-    if constexpr (PH == PH_RS) {
-      double acc = (double)in[0];
-#pragma unroll
-      for (int k = 1; k < P; ++k) acc = __dadd_rn(acc, (double)in[k]);
-      la = __double2float_rn(__dmul_rn(acc, (double)kp.scale));
-    } else {
-      la = in[0];
-    }
-  } else if constexpr (OP == OP_SGD) {
-    float G;
-    if constexpr (PH == PH_RS) {
-      double acc = (double)in[0];
-#pragma unroll
-      for (int k = 1; k < P; ++k) acc = __dadd_rn(acc, (double)in[k]);
-      G = __double2float_rn(acc);
-    } else {
-      G = in[0];
-    }
-    la = G;  // the reduced gradient is written back (R15)
-    sgd1(kp, G, lb, lc);
-  } else {  // OP_EASGD: la = x_r, lb = center
-    if constexpr (PH == PH_RS) {
-      const float xc = lb;
-      float s = 0.f, xr = in[0];
-#pragma unroll
-      for (int k = 0; k < P; ++k) {
-        const float d = __fsub_rn(in[k], xc);
-        s = (k == 0) ? d : __fadd_rn(s, d);
-        if (k == r) xr = in[k];
-      }
-      const float dr = __fsub_rn(xr, xc);
-      la = __fsub_rn(xr, __fmul_rn(kp.alpha, dr));
-      lb = __fadd_rn(xc, __fmul_rn(kp.alpha, s));
-    } else {
-      const float dr = __fsub_rn(la, lb);  // this rank's (old) center replica
-      la = __fsub_rn(la, __fmul_rn(kp.alpha, dr));
-      lb = in[0];  // the owner's new center
-    }
-  }
-}
-
-// ------------------------------------------------------------------ slot addressing
-// One lane's slot: flat slot s, element offset e inside its tensor, cnt valid elements (1..4).
-struct SlotRef {
-  int s, cnt;      // flat slot; number of valid elements (0 = inactive lane)
-  int lo_i, hi_i;  // valid element lanes [lo_i, hi_i) of the slot
-  int64_t e;       // element index of lane 0 inside its tensor (negative for a shifted head)
-  bool vec;        // full 16-B slot, 16-B aligned in every group of the call
-};
-
-// Per-lane cache of the current tensor and the NP tensor pointers the phase body needs, so the
-// steady state issues no pointer-table loads (refreshed only when a lane crosses a tensor).
-template <int NP>
-struct TensorCache {
-  int t, lo, hi, shift;
-  int64_t n;
-  bool vec;
-  float* ptr[NP];
-};
-
-// A tensor whose pointers sit m elements past a 16-B boundary on every rank (views of a flat
-// bucket with odd sizes) is laid out with its slot grid shifted by m: slot 0 holds elements
-// [0, 4-m), later slots are 16-B aligned, so it keeps the vector path.
-template <class Body>
-__device__ __forceinline__ void resolve(const KParams& kp, const Body& body,
-                                        TensorCache<Body::NP>& c, int s, SlotRef& ref) {
-  if (s < c.lo || s >= c.hi) {
-    // the slot's tensor lies between the tensors holding the first slots of its 128-slot block
-    // and of the next block: binary search there (largest t with prefix[t] <= s)
-    const int blk = s >> kPieceShift;
-    int t = __ldg(kp.block_t + blk);
-    if (__ldg(kp.prefix + t + 1) <= s) {
-      int b = __ldg(kp.block_t + blk + 1) + 1;  // prefix[b] > s
-      while (b - t > 1) {
-        const int m = (t + b) >> 1;
-        if (__ldg(kp.prefix + m) <= s) t = m; else b = m;
-      }
-    }
-    c.t = t;
-    c.lo = __ldg(kp.prefix + t);
-    c.hi = __ldg(kp.prefix + t + 1);
-    c.n = __ldg(kp.numel + t);
-    c.shift = __ldg(kp.shift + t);
-    c.vec = __ldg(kp.vec_ok + t) &&
-            (!kp.vec_ok_b || (__ldg(kp.vec_ok_b + t) && __ldg(kp.shift_b + t) == c.shift)) &&
-            (!kp.vec_ok_c || (__ldg(kp.vec_ok_c + t) && __ldg(kp.shift_c + t) == c.shift));
-    body.bind(t, c.ptr);
-  }
-  ref.s = s;
-  ref.e = (int64_t)(s - c.lo) * 4 - c.shift;
-  ref.lo_i = ref.e < 0 ? (int)(-ref.e) : 0;
-  const int64_t rem = c.n - ref.e;
-  ref.hi_i = rem >= 4 ? 4 : (int)rem;
-  ref.cnt = ref.hi_i - ref.lo_i;
-  ref.vec = c.vec && ref.cnt == 4;
-}
-
-// Tensor-structured operand at element ref.e of a tensor base pointer.
-template <bool VEC>
-__device__ __forceinline__ float4 ldv(const float* base, const SlotRef& ref) {
-  base += ref.e;
-  if constexpr (VEC) {
-    return ld16(base);
-  } else {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i >= ref.lo_i && i < ref.hi_i) lane(v, i) = ld4(base + i);
-    return v;
-  }
-}
-template <bool VEC>
-__device__ __forceinline__ void stv(float* base, const SlotRef& ref, float4 v) {
-  base += ref.e;
-  if constexpr (VEC) {
-    st16(base, v);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i >= ref.lo_i && i < ref.hi_i) st4(base + i, lane(v, i));
-  }
-}
-
-// Staging / scratch regions of the per-rank arena (flat, slot-indexed relative to a chunk).
-__device__ __forceinline__ float* arena_stage(const KParams& kp, int rank, int parity) {
-  return kp.arena[rank] + (size_t)parity * kp.chunk_cap * 4;
-}
-__device__ __forceinline__ float* arena_scratch(const KParams& kp, int rank, int src) {
-  return kp.arena[rank] + (size_t)(2 + src) * kp.chunk_cap * 4;
-}
-
-// [lo, hi) is cut into pieces of kPiece slots dealt round-robin to the CTAs of the grid (then
-// to the warps of a CTA), so at any moment the whole GPU streams one contiguous window of memory
-// (DRAM page locality: +40% over per-CTA contiguous ranges, tools/p2p_probe.cu).  The piece ->
-// CTA map depends only on (lo, hi, gridDim), so CTA b of every rank touches the same pieces of a
-// chunk -- the pairing the per-CTA flags rely on.  A lane handles U slots 32 apart per step.
-// Body: NP cached pointers filled by bind(t, ptr); load<VEC>(ref, ptr, st) issues every load
-// of a slot; finish<VEC>(ref, st) computes and stores.  All U slots' loads precede the first
-// finish.
-template <int U, class Body>
-__device__ __forceinline__ void slot_loop(const KParams& kp, int lo, int hi, const Body& body) {
-  static_assert(kPiece % (32 * U) == 0, "piece must be a multiple of a warp step");
-  const int lane_id = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int npieces = (hi - lo + kPiece - 1) / kPiece;
-  TensorCache<Body::NP> tc;
-  tc.t = -1;
-  tc.lo = tc.hi = 0;
-  for (int c = blockIdx.x + gridDim.x * warp; c < npieces; c += gridDim.x * nw) {
-    const int pbase = lo + c * kPiece;
-    const int pend = min(hi, pbase + kPiece);
-#pragma unroll 1
-    for (int step = pbase; step < pend; step += 32 * U) {
-      SlotRef ref[U];
-      typename Body::State st[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int s = step + lane_id + 32 * u;
-        if (s < pend) {
-          resolve(kp, body, tc, s, ref[u]);
-          if (ref[u].vec) body.template load<true>(ref[u], tc.ptr, st[u]);
-          else body.template load<false>(ref[u], tc.ptr, st[u]);
-        } else {
-          ref[u].cnt = 0;
-          ref[u].vec = false;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (ref[u].vec) body.template finish<true>(ref[u], st[u]);
-        else if (ref[u].cnt) body.template finish<false>(ref[u], st[u]);
-      }
-    }
-  }
-}
-
-// Small groups: one slot per thread, threads of the grid in order (consecutive threads,
-// consecutive slots), so every slot's tensor lookup runs in parallel instead of a warp walking
-// a piece of many tiny tensors serially.
-template <class Body>
-__device__ __forceinline__ void slot_loop_flat(const KParams& kp, int lo, int hi,
-                                               const Body& body) {
-  TensorCache<Body::NP> tc;
-  tc.t = -1;
-  tc.lo = tc.hi = 0;
-  const int stride = gridDim.x * blockDim.x;
-  for (int s = lo + blockIdx.x * blockDim.x + threadIdx.x; s < hi; s += stride) {
-    SlotRef ref;
-    typename Body::State st;
-    resolve(kp, body, tc, s, ref);
-    if (ref.vec) {
-      body.template load<true>(ref, tc.ptr, st);
-      body.template finish<true>(ref, st);
-    } else {
-      body.template load<false>(ref, tc.ptr, st);
-      body.template finish<false>(ref, st);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ phase bodies
-enum SrcKind {
-  SRC_TENSORS = 0,   // every rank's primary tensor (pull reduce-scatter, local path)
-  SRC_SCRATCH = 1,   // own primary tensor for k == r, else own receive scratch of rank k (push)
-  SRC_ONESHOT = 2,   // every rank's one-shot staging buffer (flat over the whole group)
-};
-
-// Reduce P sources, apply the epilogue to this rank's operands; optionally also write the
-// reduced primary value into this rank's staging chunk (for the staged allgather).
-// Cached pointers: [0..2] = this rank's a, b, c tensors, then (SRC_TENSORS) P source tensors.
-template <int OP, int P, int SRC, bool STAGE_OUT>
-struct ReduceBody {
-  using N = Needs<OP, PH_RS, P>;
-  static constexpr int NP = 3 + (SRC == SRC_TENSORS ? P : 0);
-  const KParams& kp;
-  int r;
-  int origin;         // first slot of the chunk (flat offsets of staging / scratch)
-  float* stage_out;   // this rank's staging chunk (STAGE_OUT)
-  struct State {
-    float4 x[P];
-    float4 b, c;
-    float *pa, *pb, *pc;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const {
-    const size_t mine = (size_t)r * kp.T + t;
-    ptr[0] = kp.a[mine];
-    ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
-    ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
-    if constexpr (SRC == SRC_TENSORS) {
-      // P == 1 (local paths): the single source is this rank's own tensor
-#pragma unroll
-      for (int k = 0; k < P; ++k) ptr[3 + k] = kp.a[(size_t)(P == 1 ? r : k) * kp.T + t];
-    }
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      if constexpr (SRC == SRC_TENSORS) {
-        st.x[k] = ldv<VEC>(ptr[3 + k], ref);
-      } else if constexpr (SRC == SRC_SCRATCH) {
-        st.x[k] = (k == r) ? ldv<VEC>(ptr[0], ref)
-                           : ld16(arena_scratch(kp, r, k) + (size_t)(ref.s - origin) * 4);
-      } else {
-        st.x[k] = ld16(kp.stage[k] + stage_off() + (size_t)ref.s * 4);
-      }
-    }
-    if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
-    if constexpr (N::loadC) st.c = ldv<VEC>(ptr[2], ref);
-    st.pa = ptr[0];
-    st.pb = ptr[1];
-    st.pc = ptr[2];
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-    float4 oa;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float in[P];
-#pragma unroll
-      for (int k = 0; k < P; ++k) in[k] = lane(st.x[k], i);
-      float la = 0.f;
-      float lb = N::loadB ? lane(st.b, i) : 0.f;
-      float lc = N::loadC ? lane(st.c, i) : 0.f;
-      elem<OP, PH_RS, P>(kp, r, in, la, lb, lc);
-      lane(oa, i) = la;
-      if constexpr (N::storeB) lane(st.b, i) = lb;
-      if constexpr (N::storeC) lane(st.c, i) = lc;
-    }
-    if constexpr (N::storeA) stv<VEC>(st.pa, ref, oa);
-    if constexpr (N::storeB) stv<VEC>(st.pb, ref, st.b);
-    if constexpr (N::storeC) stv<VEC>(st.pc, ref, st.c);
-    if constexpr (STAGE_OUT) {
-      // EASGD gathers the owner's new center, the other ops the reduced primary value
-      st16(stage_out + (size_t)(ref.s - origin) * 4, OP == OP_EASGD ? st.b : oa);
-    }
-  }
-};
-
-// Allgather: take owner q's staged value, apply the epilogue to this rank's operands.
-template <int OP>
-struct GatherBody {
-  using N = Needs<OP, PH_AG, 2>;
-  static constexpr int NP = 3;
-  const KParams& kp;
-  int r;
-  int origin;
-  const float* src;   // owner's staging chunk
-  struct State {
-    float4 x, a, b, c;
-    float *pa, *pb, *pc;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const {
-    const size_t mine = (size_t)r * kp.T + t;
-    ptr[0] = kp.a[mine];
-    ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
-    ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
-    st.x = ld16(src + (size_t)(ref.s - origin) * 4);
-    if constexpr (N::loadA) st.a = ldv<VEC>(ptr[0], ref);
-    if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
-    if constexpr (N::loadC) st.c = ldv<VEC>(ptr[2], ref);
-    st.pa = ptr[0];
-    st.pb = ptr[1];
-    st.pc = ptr[2];
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float in[1] = {lane(st.x, i)};
-      float la = N::loadA ? lane(st.a, i) : 0.f;
-      float lb = N::loadB ? lane(st.b, i) : 0.f;
-      float lc = N::loadC ? lane(st.c, i) : 0.f;
-      elem<OP, PH_AG, 2>(kp, r, in, la, lb, lc);
-      lane(st.a, i) = la;
-      if constexpr (N::storeB) lane(st.b, i) = lb;
-      if constexpr (N::storeC) lane(st.c, i) = lc;
-    }
-    stv<VEC>(st.pa, ref, st.a);
-    if constexpr (N::storeB) stv<VEC>(st.pb, ref, st.b);
-    if constexpr (N::storeC) stv<VEC>(st.pc, ref, st.c);
-  }
-};
-
-// Copy this rank's primary tensors into a flat destination (push to an owner's scratch, or
-// the one-shot staging buffer).
-struct CopyOutBody {
-  static constexpr int NP = 1;
-  const KParams& kp;
-  int r;
-  int origin;
-  float* dst;
-  struct State {
-    float4 x;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const {
-    ptr[0] = kp.a[(size_t)r * kp.T + t];
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
-    st.x = ldv<VEC>(ptr[0], ref);
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-    st16(dst + (size_t)(ref.s - origin) * 4, st.x);
-  }
-};
-
-// Slots per lane per step: enough independent 16-B loads in flight within the register budget
-// of MINB resident 512-thread CTAs per SM.
-__host__ __device__ constexpr int unroll_for(int nsrc, int minb) {
-  return minb >= 2 ? (nsrc <= 2 ? 2 : 1) : (nsrc <= 2 ? 4 : (nsrc <= 4 ? 2 : 1));
-}
-
-// Whole CTA: wait until rank q's CTA has passed `bar`.  Returns false on timeout.
-__device__ bool wait_one(const KParams& kp, int r, int q, int bar) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) {
-    int ok = 1;
-    const uint32_t* mine = kp.flags[r] + flag_index(bar, q, blockIdx.x);
-    if ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
-      const unsigned long long t0 = globaltimer();
-      while ((int32_t)(ld_acquire_sys(mine) - ep()) < 0) {
-        if (globaltimer() - t0 > kp.timeout_ns) {
-          atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
-          ok = 0;
-          break;
-        }
-      }
-    }
-    s_ok = ok;
-  }
-  __syncthreads();
-  const int ok = s_ok;
-  __syncthreads();
-  return ok != 0;
-}
-
-// Staged allgather: once every peer's CTA has staged its chunk (one barrier, so all CTAs start
-// together), pull the other owners' chunks r+1, r+2, ... in turn.  At each step the ranks read
-// from a permutation of the owners, the NVLink pattern B200 serves fastest.  Measured at p = 4
-// (ResNet-50): barrier + rank rotation 117 us; per-owner waits (CTAs drift apart and the steps
-// mix) 131-156 us; owners mixed per CTA 134-154 us; "whichever owner is ready first" 155-182 us.
-template <int OP, int P, int MINB>
-__device__ __forceinline__ bool gather_all(const KParams& kp, int r, int par) {
-  const int64_t M = kp.M;
-  if (!barrier_all(kp, r, BAR_MID, true)) return false;
-#pragma unroll 1
-  for (int j = 0; j < P - 1; ++j) {
-    const int q = (r + 1 + j) % P;
-    const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
-    GatherBody<OP> body{kp, r, lo, arena_stage(kp, q, par)};
-    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
-  }
-  return true;
-}
-
-// ------------------------------------------------------------------ NVLS (switch reduction)
-// multimem.ld_reduce on a multicast address returns the sum of every rank's copy, reduced in
-// the NVSwitch (fp32, order chosen by the switch); multimem.st writes every rank's copy.
-__device__ __forceinline__ float4 mm_ld_reduce16(const float* p) {
-  float4 v;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ float mm_ld_reduce4(const float* p) {
-  float v;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void mm_st16(float* p, float4 v) {
-  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void mm_st4(float* p, float v) {
-  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
-// Owner side of NVLS: reduce every rank's copy of an owned slot in the switch, apply the
-// allreduce scale, multicast-store the result into every rank's copy.
-template <int OP>
-struct NvlsBody {
-  static constexpr int NP = 1;
-  const KParams& kp;
-  int r;
-  struct State {
-    float4 v;
-    float* mp;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const { ptr[0] = kp.mc[t]; }
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
-    st.mp = ptr[0] + ref.e;
-    if constexpr (VEC) {
-      st.v = mm_ld_reduce16(st.mp);
-    } else {
-      st.v = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i >= ref.lo_i && i < ref.hi_i) lane(st.v, i) = mm_ld_reduce4(st.mp + i);
-    }
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-    if constexpr (OP == OP_ALLREDUCE) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        lane(st.v, i) = __double2float_rn(__dmul_rn((double)lane(st.v, i), (double)kp.scale));
-    }
-    if constexpr (VEC) {
-      mm_st16(st.mp, st.v);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i >= ref.lo_i && i < ref.hi_i) mm_st4(st.mp + i, lane(st.v, i));
-    }
-  }
-};
-
-// ------------------------------------------------------------------ low-latency (LL)
-// Rank r's words for peer k live in k's LL buffer [parity][source r][4*slot + lane]: 8 bytes =
-// {epoch, value bits}.  8-byte stores are single-copy atomic, so a reader that sees the current
-// epoch in a word also sees that word's value -- no separate flag, no barrier.  The parity half
-// a call writes was last read two calls ago, which every peer finished before this call began.
-__device__ __forceinline__ unsigned long long* ll_buf(const KParams& kp, int rank, int par,
-                                                      int src) {
-  return reinterpret_cast<unsigned long long*>(kp.stage[rank] + 2 * (kStageCapacity / sizeof(float))) +
-         ((size_t)par * kp.p + src) * (size_t)kp.ll_cap;
-}
-__device__ __forceinline__ void st_ll(unsigned long long* p, float a, float b, uint32_t e) {
-  const unsigned long long x = ((unsigned long long)e << 32) | __float_as_uint(a);
-  const unsigned long long y = ((unsigned long long)e << 32) | __float_as_uint(b);
-  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
-}
-__device__ __forceinline__ void ld_ll(const unsigned long long* p, unsigned long long& x,
-                                      unsigned long long& y) {
-  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
-}
-
-template <int OP, int P>
-struct LLBody {
-  using N = Needs<OP, PH_RS, P>;
-  static constexpr int NP = 3;
-  const KParams& kp;
-  int r;
-  int par;
-  struct State {
-    float4 own, b, c;
-    float *pa, *pb, *pc;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const {
-    const size_t mine = (size_t)r * kp.T + t;
-    ptr[0] = kp.a[mine];
-    ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
-    ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
-  }
-  // Issue the local loads and push this slot to every peer.
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
-    st.own = ldv<VEC>(ptr[0], ref);
-    if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
-    if constexpr (N::loadC) st.c = ldv<VEC>(ptr[2], ref);
-    st.pa = ptr[0];
-    st.pb = ptr[1];
-    st.pc = ptr[2];
-    const uint32_t e = ep();
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      if (k == r) continue;
-      unsigned long long* dst = ll_buf(kp, k, par, r) + 4 * (size_t)ref.s;
-      st_ll(dst, st.own.x, st.own.y, e);
-      st_ll(dst + 2, st.own.z, st.own.w, e);
-    }
-  }
-  // Wait for every peer's words of this slot, reduce in rank order, apply the epilogue.
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-    const uint32_t e = ep();
-    float4 in[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      if (k == r) {
-        in[k] = st.own;
-        continue;
-      }
-      const unsigned long long* src = ll_buf(kp, r, par, k) + 4 * (size_t)ref.s;
-      unsigned long long x0, x1, x2, x3;
-      unsigned long long t0 = 0;
-      while (true) {
-        ld_ll(src, x0, x1);
-        ld_ll(src + 2, x2, x3);
-        if ((uint32_t)(x0 >> 32) == e && (uint32_t)(x1 >> 32) == e && (uint32_t)(x2 >> 32) == e &&
-            (uint32_t)(x3 >> 32) == e)
-          break;
-        if (t0 == 0) t0 = globaltimer();
-        else if (globaltimer() - t0 > kp.timeout_ns) {
-          atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
-          break;
-        }
-      }
-      in[k] = make_float4(__uint_as_float((uint32_t)x0), __uint_as_float((uint32_t)x1),
-                          __uint_as_float((uint32_t)x2), __uint_as_float((uint32_t)x3));
-    }
-    float4 oa;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float v[P];
-#pragma unroll
-      for (int k = 0; k < P; ++k) v[k] = lane(in[k], i);
-      float la = 0.f;
-      float lb = N::loadB ? lane(st.b, i) : 0.f;
-      float lc = N::loadC ? lane(st.c, i) : 0.f;
-      elem<OP, PH_RS, P>(kp, r, v, la, lb, lc);
-      lane(oa, i) = la;
-      if constexpr (N::storeB) lane(st.b, i) = lb;
-      if constexpr (N::storeC) lane(st.c, i) = lc;
-    }
-    if constexpr (N::storeA) stv<VEC>(st.pa, ref, oa);
-    if constexpr (N::storeB) stv<VEC>(st.pb, ref, st.b);
-    if constexpr (N::storeC) stv<VEC>(st.pc, ref, st.c);
-  }
-};
-
-// ------------------------------------------------------------------ kernels
-template <int OP, int P, int MINB>
-__global__ void __launch_bounds__(512, MINB) k_twoshot_pull(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  const int par = (int)(ep() & 1u);
-  const int64_t M = kp.M;
-  stamp(kp, 0);
-  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
-  stamp(kp, 1);
-  const int lo = (int)(M * r / P), hi = (int)(M * (r + 1) / P);
-  {
-    ReduceBody<OP, P, SRC_TENSORS, true> body{kp, r, lo, arena_stage(kp, r, par)};
-    slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
-  }
-  stamp(kp, 2);
-  stamp(kp, 3);
-  if (!gather_all<OP, P, MINB>(kp, r, par)) return;
-  stamp(kp, 4);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
-template <int OP, int P, int MINB>
-__global__ void __launch_bounds__(512, MINB) k_twoshot_push(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  const int par = (int)(ep() & 1u);
-  const int64_t M = kp.M;
-  stamp(kp, 0);
-  // push my contribution to this CTA's pieces of every other chunk into its owner's scratch
-#pragma unroll 1
-  for (int j = 1; j < P; ++j) {
-    const int q = (r + j) % P;
-    const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
-    CopyOutBody body{kp, r, lo, arena_scratch(kp, q, r)};
-    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
-    __syncthreads();
-    if (threadIdx.x == 0) signal_one(kp, BAR_ENTRY, r, q);
-  }
-  stamp(kp, 1);
-  if (!barrier_all(kp, r, BAR_ENTRY, false)) return;  // every peer's push has landed
-  const int lo = (int)(M * r / P), hi = (int)(M * (r + 1) / P);
-  {
-    ReduceBody<OP, P, SRC_SCRATCH, true> body{kp, r, lo, arena_stage(kp, r, par)};
-    slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
-  }
-  stamp(kp, 2);
-  stamp(kp, 3);
-  if (!gather_all<OP, P, MINB>(kp, r, par)) return;
-  stamp(kp, 4);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
-template <int OP, int P, int MINB>
-__global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  const int lo = 0, hi = kp.M;
-  stamp(kp, 0);
-  {
-    CopyOutBody body{kp, r, 0, kp.stage[r] + stage_off()};
-    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
-  }
-  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
-  stamp(kp, 1);
-  ReduceBody<OP, P, SRC_ONESHOT, false> body{kp, r, 0, nullptr};
-  slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
-// Low-latency: no barrier; each slot is pushed to every peer and its peers' words awaited.
-template <int OP, int P, int MINB>
-__global__ void __launch_bounds__(512, MINB) k_ll(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  stamp(kp, 0);
-  LLBody<OP, P> body{kp, r, (int)(ep() & 1u)};
-  slot_loop_flat(kp, 0, kp.M, body);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
-// NVLS: ENTRY barrier -> owner slots reduced in the switch and multicast back -> MID barrier
-// (every owner's stores landed everywhere) -> SGD epilogue over this CTA's pieces of every
-// chunk from local memory.  Per GPU: ~(1 + 1/p) S of NVLink traffic each way.
-template <int OP, int P, int MINB>
-__global__ void __launch_bounds__(512, MINB) k_nvls(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  const int64_t M = kp.M;
-  stamp(kp, 0);
-  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
-  stamp(kp, 1);
-  {
-    NvlsBody<OP> body{kp, r};  // small state: 4 switch reductions in flight per lane
-    slot_loop<4>(kp, (int)(M * r / P), (int)(M * (r + 1) / P), body);
-  }
-  __threadfence_system();
-  stamp(kp, 2);
-  if constexpr (OP == OP_SGD) {
-    // epilogue: my own chunk first, then every other chunk as soon as its owner's CTA is done
-    signal_all(kp, r, BAR_MID);
-    auto epi = [&](int q) {
-      ReduceBody<OP_SGD, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
-      slot_loop<unroll_for(1, MINB)>(kp, (int)(M * q / P), (int)(M * (q + 1) / P), body);
-    };
-    epi(r);
-    stamp(kp, 3);
-#pragma unroll 1
-    for (int j = 0; j < P - 1; ++j) {
-      const int q = (r + 1 + j) % P;
-      if (!wait_one(kp, r, q, BAR_MID)) return;
-      epi(q);
-    }
-  } else {
-    // the result must have landed everywhere before the kernel (the call) completes
-    if (!barrier_all(kp, r, BAR_MID, true)) return;
-    stamp(kp, 3);
-  }
-  stamp(kp, 4);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
-template <int OP, int MINB, int U>
-__global__ void __launch_bounds__(512, MINB) k_local(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  ReduceBody<OP, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
-  slot_loop<U>(kp, 0, kp.M, body);
-}
-
-// p = 1, lean variant: a piece (128 slots) that lies inside one tensor and is made of full,
-// aligned 16-B slots -- almost every piece of a real gradient group -- is streamed with
-// warp-uniform affine addresses (no per-slot lookup, few registers); only pieces that straddle a
-// tensor boundary or hold a partial/unaligned slot take the generic per-slot path.
-template <int OP, int U>
-__device__ __forceinline__ void local_fast_piece(const KParams& kp, int r, float* pa, float* pb,
-                                                 float* pc, int ln, int nslots) {
-  using N = Needs<OP, PH_RS, 1>;
-#pragma unroll 1
-  for (int base = 0; base < nslots; base += 32 * U) {
-    float4 va[U], vb[U], vc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + ln + 32 * u;
-      if (i < nslots) {
-        va[u] = ld16(pa + 4 * (size_t)i);
-        if constexpr (N::loadB) vb[u] = ld16(pb + 4 * (size_t)i);
-        if constexpr (N::loadC) vc[u] = ld16(pc + 4 * (size_t)i);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + ln + 32 * u;
-      if (i < nslots) {
-        float4 oa;
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          const float in[1] = {lane_of(va[u], l)};
-          float la = 0.f;
-          float lb = N::loadB ? lane_of(vb[u], l) : 0.f;
-          float lc = N::loadC ? lane_of(vc[u], l) : 0.f;
-          elem<OP, PH_RS, 1>(kp, r, in, la, lb, lc);
-          lane(oa, l) = la;
-          if constexpr (N::storeB) lane(vb[u], l) = lb;
-          if constexpr (N::storeC) lane(vc[u], l) = lc;
-        }
-        if constexpr (N::storeA) st16(pa + 4 * (size_t)i, oa);
-        if constexpr (N::storeB) st16(pb + 4 * (size_t)i, vb[u]);
-        if constexpr (N::storeC) st16(pc + 4 * (size_t)i, vc[u]);
-      }
-    }
-  }
-}
-
-template <int OP, int MINB, int U>
-__global__ void __launch_bounds__(512, MINB) k_local_lean(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  const int lane_id = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int M = kp.M;
-  const int npieces = (M + kPiece - 1) / kPiece;
-  ReduceBody<OP, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
-  TensorCache<ReduceBody<OP, 1, SRC_TENSORS, false>::NP> tc;
-  tc.t = -1;
-  tc.lo = tc.hi = 0;
-  for (int c = blockIdx.x + gridDim.x * warp; c < npieces; c += gridDim.x * nw) {
-    const int pbase = c * kPiece;
-    const int pend = min(M, pbase + kPiece);
-    SlotRef r0;
-    resolve(kp, body, tc, pbase, r0);  // warp-uniform: every lane resolves the same slot
-    if (tc.vec && r0.e >= 0 && pend <= tc.hi && (int64_t)(pend - tc.lo) * 4 - tc.shift <= tc.n) {
-      local_fast_piece<OP, U>(kp, r, tc.ptr[0] + r0.e, tc.ptr[1] ? tc.ptr[1] + r0.e : nullptr,
-                              tc.ptr[2] ? tc.ptr[2] + r0.e : nullptr, lane_id, pend - pbase);
-      continue;
-    }
-#pragma unroll 1
-    for (int s = pbase + lane_id; s < pend; s += 32) {
-      SlotRef ref;
-      typename ReduceBody<OP, 1, SRC_TENSORS, false>::State st;
-      resolve(kp, body, tc, s, ref);
-      if (ref.vec) {
-        body.template load<true>(ref, tc.ptr, st);
-        body.template finish<true>(ref, st);
-      } else {
-        body.template load<false>(ref, tc.ptr, st);
-        body.template finish<false>(ref, st);
-      }
-    }
-  }
-}
-
-template <int OP>
-const void* kernel_ptr(int algo, int p, int variant) {
-  if (algo == ALGO_LOCAL) {
-    switch (variant) {
-      // measured (ResNet-50 group, fused SGD): lean 1 CTA/SM U=4 87.5 us, lean 2/SM U=2 89.2,
-      // generic 2/SM U=2 88.0, generic 1/SM U=4 110.7
-      case 1: return (const void*)k_local<OP, 1, 4>;
-      case 2: return (const void*)k_local<OP, 2, 2>;
-      case 3: return (const void*)k_local_lean<OP, 2, 4>;
-      case 4: return (const void*)k_local_lean<OP, 2, 2>;
-      default: return (const void*)k_local_lean<OP, 1, 4>;
-    }
-  }
-#define TC_CASE(PP)                                                                  \
-  case PP:                                                                           \
-    if constexpr (OP != OP_EASGD)                                                    \
-      if (algo == ALGO_NVLS)                                                         \
-        return variant == 1 ? (const void*)k_nvls<OP, PP, 1> : (const void*)k_nvls<OP, PP, 2>; \
-    if (algo == ALGO_NVLS) return nullptr;                                           \
-    if (algo == ALGO_LL)                                                             \
-      return variant == 1 ? (const void*)k_ll<OP, PP, 1> : (const void*)k_ll<OP, PP, 2>; \
-    if (variant == 1)                                                                \
-      return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 1>           \
-           : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 1>      \
-                                       : (const void*)k_oneshot<OP, PP, 1>;          \
-    return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 2>             \
-         : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 2>        \
-                                     : (const void*)k_oneshot<OP, PP, 2>;
-  switch (p) {
-    TC_CASE(2) TC_CASE(3) TC_CASE(4) TC_CASE(5) TC_CASE(6) TC_CASE(7) TC_CASE(8)
-    default: return nullptr;
-  }
-#undef TC_CASE
-}
-
 const void* select_kernel(int op, int algo, int p, int variant) {
   switch (op) {
-    case OP_ALLREDUCE: return kernel_ptr<OP_ALLREDUCE>(algo, p, variant);
-    case OP_SGD: return kernel_ptr<OP_SGD>(algo, p, variant);
-    case OP_EASGD: return kernel_ptr<OP_EASGD>(algo, p, variant);
+    case OP_ALLREDUCE: return kernel_ptr_allreduce(algo, p, variant);
+    case OP_SGD: return kernel_ptr_sgd(algo, p, variant);
+    case OP_EASGD: return kernel_ptr_easgd(algo, p, variant);
   }
   return nullptr;
 }

@@ -26,6 +26,13 @@ constexpr int64_t kDefaultLLMax = 1 << 20;
 constexpr int64_t kDefaultOneshotMax = 256 << 10;
 constexpr int kPieceShift = 7;                 // work piece = 128 slots = 2 KiB per operand
 constexpr int kPiece = 1 << kPieceShift;
+// p = 1 TMA stream (k_local_tma): tiles of up to kTileE elements inside one tensor, kTmaStages
+// shared-memory stages of (up to) three operands, one producer warp + kTmaConsumerWarps.
+constexpr int kTileE = 2048;
+constexpr int kTmaStages = 4;
+constexpr int kTmaConsumerWarps = 8;
+constexpr int kTmaThreads = 32 * (1 + kTmaConsumerWarps);
+constexpr int kTmaSmem = kTmaStages * 3 * kTileE * 4;
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
@@ -100,6 +107,8 @@ struct KParams {
   int* err;              // host-mapped sticky error word
   int absent_rank;       // fault injection (emulated only), -1 off
   unsigned long long* prof; // optional per-CTA phase timestamps [nlocal*ctas][8] (ns)
+  const int4* tiles;     // p = 1 TMA stream: {tensor, first element, elements, 0} per tile
+  int ntiles;
 };
 
 // Kernel launchers (tc_kernels.cu).
@@ -179,6 +188,8 @@ struct Group {
   std::vector<std::pair<int, std::string>> mapped_keys;  // ipc_cache keys held
   std::vector<float*> h_mc;      // [T] multicast addresses (NVLS-eligible groups only)
   float** d_mc = nullptr;
+  int4* d_tiles = nullptr;       // p = 1: tile table of the TMA stream (k_local_tma)
+  int ntiles = 0;
 };
 
 }  // namespace tc

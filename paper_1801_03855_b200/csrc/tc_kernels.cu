@@ -17,13 +17,25 @@ const void* select_kernel(int op, int algo, int p, int variant) {
   return nullptr;
 }
 
+// The p = 1 TMA stream (variant 0 of ALGO_LOCAL) runs kTmaThreads threads with kTmaSmem bytes
+// of dynamic shared memory.
+bool is_tma(int algo, int variant) { return algo == ALGO_LOCAL && variant == 0; }
+
+cudaError_t prepare(const void* k, int algo, int variant) {
+  if (!is_tma(algo, variant)) return cudaSuccess;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+}
+
 }  // namespace
 
 int max_ctas_per_sm(int op, int algo, int p, int threads, int variant) {
   const void* k = select_kernel(op, algo, p, variant);
-  if (!k) return 0;
+  if (!k || prepare(k, algo, variant) != cudaSuccess) return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, 0) != cudaSuccess) return 0;
+  const bool tma = is_tma(algo, variant);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, tma ? kTmaThreads : threads,
+                                                    tma ? kTmaSmem : 0) != cudaSuccess)
+    return 0;
   return n;
 }
 
@@ -31,11 +43,15 @@ cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int thread
                        bool cooperative, cudaStream_t stream, int variant) {
   const void* k = select_kernel(op, algo, kp.p, variant);
   if (!k) return cudaErrorInvalidValue;
+  cudaError_t e = prepare(k, algo, variant);
+  if (e != cudaSuccess) return e;
   KParams arg = kp;
   void* args[] = {&arg};
-  dim3 grid(ctas, nlocal), block(threads);
-  if (cooperative) return cudaLaunchCooperativeKernel(k, grid, block, args, 0, stream);
-  return cudaLaunchKernel(k, grid, block, args, 0, stream);
+  const bool tma = is_tma(algo, variant);
+  dim3 grid(ctas, nlocal), block(tma ? kTmaThreads : threads);
+  const size_t smem = tma ? kTmaSmem : 0;
+  if (cooperative) return cudaLaunchCooperativeKernel(k, grid, block, args, smem, stream);
+  return cudaLaunchKernel(k, grid, block, args, smem, stream);
 }
 
 }  // namespace tc

@@ -150,6 +150,9 @@ void free_group_device(Group& g) {
   g.d_shift = nullptr;
   cudaFree(g.d_mc);
   g.d_mc = nullptr;
+  cudaFree(g.d_tiles);
+  g.d_tiles = nullptr;
+  g.ntiles = 0;
   g.d_ptrs = nullptr;
   g.d_prefix = nullptr;
   g.d_block_t = nullptr;
@@ -200,6 +203,29 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
   TC_CUDA(cudaMemcpy(g.d_vec_ok, vec_ok.data(), vec_ok.size(), cudaMemcpyHostToDevice));
   TC_CUDA(cudaMalloc((void**)&g.d_shift, g.shift.size()));
   TC_CUDA(cudaMemcpy(g.d_shift, g.shift.data(), g.shift.size(), cudaMemcpyHostToDevice));
+  if (g.comm->nranks == 1) {
+    // p = 1 TMA stream: tiles of <= kTileE elements inside one tensor, starting on the
+    // tensor's first 16-B boundary (the head before it, and the last (n - head) % 4 elements,
+    // are tiles of their own on the element path).  The other operands take the vector path
+    // when they share the misalignment (checked per tile in the kernel).
+    std::vector<int4> tiles;
+    for (int t = 0; t < pl.T; ++t) {
+      const int64_t n = pl.numel[(size_t)t];
+      const int64_t head = std::min<int64_t>(n, (4 - g.shift[(size_t)t]) & 3);
+      const int64_t full = head + ((n - head) & ~(int64_t)3);
+      if (head > 0) tiles.push_back(make_int4(t, 0, (int)head, 0));
+      for (int64_t e = head; e < full; e += kTileE)
+        tiles.push_back(make_int4(t, (int)e, (int)std::min<int64_t>(kTileE, full - e), 0));
+      if (full < n) tiles.push_back(make_int4(t, (int)full, (int)(n - full), 0));
+    }
+    if (tiles.size() >= (size_t)INT32_MAX) return TC_ERR_INVALID_ARG;
+    g.ntiles = (int)tiles.size();
+    if (g.ntiles) {
+      TC_CUDA(cudaMalloc((void**)&g.d_tiles, sizeof(int4) * tiles.size()));
+      TC_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(int4) * tiles.size(),
+                         cudaMemcpyHostToDevice));
+    }
+  }
   if (!g.h_mc.empty()) {
     TC_CUDA(cudaMalloc((void**)&g.d_mc, sizeof(float*) * g.h_mc.size()));
     TC_CUDA(cudaMemcpy(g.d_mc, g.h_mc.data(), sizeof(float*) * g.h_mc.size(),
@@ -355,7 +381,12 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   int64_t work_slots = twoshot ? (Mdev + p - 1) / p : Mdev;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
-  if (algo == ALGO_LOCAL) {
+  if (algo == ALGO_LOCAL && c.variant == 0) {  // TMA stream
+    ctas = std::min(ga->ntiles, c.tune_ctas > 0 ? std::min(c.tune_ctas, c.num_sms * occ)
+                                                : c.num_sms * occ);
+    kp.tiles = ga->d_tiles;
+    kp.ntiles = ga->ntiles;
+  } else if (algo == ALGO_LOCAL) {
     ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * occ);
   } else if (twoshot && c.tune_ctas > 0) {
     ctas = c.tune_ctas;
@@ -379,7 +410,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   }
   c.last_algo = algo;
   c.last_ctas = ctas;
-  c.last_threads = threads;
+  c.last_threads = (algo == ALGO_LOCAL && c.variant == 0) ? kTmaThreads : threads;
   return TC_OK;
 }
 

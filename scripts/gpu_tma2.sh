@@ -1,0 +1,7 @@
+export TC_TIMEOUT_MS=10000
+timeout 300 python tools/local_tma_ctas.py resnet50
+timeout 300 python tools/local_tma_ctas.py vgg16
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for i in 1 2; do
+timeout 300 python bench.py --steps 200 --warmup 10 --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('N1', round(d['t_us'],1), round(d['roofline']['frac'],3), d['easgd']['t_us'])"
+done

@@ -95,7 +95,7 @@ def test_random_groups_grad_values(p, name, oneshot):
 
 
 @pytest.mark.parametrize("offset", [1, 2, 3, "per-rank"])
-@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("p", [1, 2, 4])
 def test_unaligned_tensors(p, offset):
     """Tensors starting 1-3 elements past a 16-B boundary.  Same misalignment on every rank:
     shifted slot grid, vector path.  Misalignment differing by rank: scalar path."""
@@ -108,11 +108,12 @@ def test_unaligned_tensors(p, offset):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
 
 
-def test_sgd_mixed_alignment():
+@pytest.mark.parametrize("p", [1, 3])
+def test_sgd_mixed_alignment(p):
     """g as views of one flat buffer (odd sizes: misaligned), w and dw separate allocations:
-    the primary grid is shifted, the other operands fall back to the scalar path."""
-    p = 3
-    numels = [7, 13, 1000, 4097, 3]
+    the primary grid is shifted, the other operands fall back to the scalar path (p = 1: the
+    TMA stream's element path for tiles misaligned in any operand)."""
+    numels = [7, 13, 1000, 4097, 3, 2048, 6001]
     gs = [W.group(numels, "grad", 70, 0, k, W.GRAD) for k in range(p)]
     w = W.group(numels, "param", 70, 0, 0, W.PARAM)
     dw = W.group(numels, "dw", 70, 0, 0, W.DW)
@@ -121,7 +122,8 @@ def test_sgd_mixed_alignment():
     dg = [list(torch.split(f, numels)) for f in flats]
     dwt = [to_dev(w) for _ in range(p)]
     ddw = [to_dev(dw, offset=2) for _ in range(p)]
-    G, Wg, D = tc.Group(comm, dg), tc.Group(comm, dwt), tc.Group(comm, ddw)
+    pick = (lambda x: x) if p > 1 else (lambda x: x[0])
+    G, Wg, D = tc.Group(comm, pick(dg)), tc.Group(comm, pick(dwt)), tc.Group(comm, pick(ddw))
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 384)
     tc.sgd_step(Wg, G, D, **hp)
     Gw, Ws, Dws = O.sgd_step([w] * p, gs, [dw] * p, **hp)
@@ -173,6 +175,17 @@ def test_single_rank_scale():
     out, algo = run_allreduce(xs, scale=0.37)
     assert algo == "local"
     assert_bitwise(out[0], O.allreduce(xs, 0.37))
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2])
+def test_single_rank_tile_boundaries(offset):
+    """p = 1 TMA stream: tensors around the 2048-element tile size, several tiles per tensor,
+    ragged tails, 1-2 element tensors; aligned (offset 0) and shifted starts."""
+    numels = [2048, 2047, 2049, 4096, 4099, 1, 2, 3, 10000, 6143, 12288]
+    xs = [W.group(numels, "grad", 79, 0, 0, W.GRAD)]
+    out, algo = run_allreduce(xs, scale=0.25, offset=offset)
+    assert algo == "local"
+    assert_bitwise(out[0], O.allreduce(xs, 0.25))
 
 
 def test_repeated_calls_epochs():
@@ -292,6 +305,26 @@ def test_easgd(name, oneshot, alpha):
         assert_bitwise(res[i][1], wc, f"center replica {i}")
 
 
+@pytest.mark.parametrize("xoff,coff", [(0, 0), (1, 1), (0, 3)])
+def test_easgd_single_client_tiles(xoff, coff):
+    """c = 1 on the p = 1 TMA stream: tile-boundary shapes, x and center shifted alike (vector
+    path) or differently (element path)."""
+    numels = [2048, 2049, 4099, 1, 10000, 6143]
+    center = W.group(numels, "center", W.CFG_EASGD, 1, 0, W.CENTER)
+    x = W.client_params(numels, center, W.CFG_EASGD, 1, 0)
+    comm = tc.Comm.single(0)
+    dx, dc = to_dev(x, offset=xoff), to_dev(center, offset=coff)
+    X, C = tc.Group(comm, dx), tc.Group(comm, dc)
+    tc.easgd_update(X, C, 0.1)
+    assert comm.last_launch()[0] == "local"
+    wx, wc = O.easgd_update([x], center, 0.1)
+    assert_bitwise(to_host(dx), wx[0], "x")
+    assert_bitwise(to_host(dc), wc, "center")
+    X.destroy()
+    C.destroy()
+    comm.destroy()
+
+
 def test_tiny_config_easgd_int_conservation():
     """Config 1's EASGD step (4 workers = 4 clients, alpha = 0.1) on integer inputs, plus the
     alpha = 0.5 conservation pin on the GPU result itself."""
@@ -374,7 +407,7 @@ def test_full_size_groups_sampled(group, p, oneshot):
     _sampled_check(numels, out, xs, 1.0 / p, p)
 
 
-@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("p", [1, 2, 4])
 @pytest.mark.parametrize("T", [1, 2, 8, 32, 161, 512, 1024])
 def test_config5_sweep_shapes(p, T):
     """Config 5 shapes (seeded log-uniform splits, unaligned tails) at the small totals the
@@ -384,13 +417,13 @@ def test_config5_sweep_shapes(p, T):
         if not numels:
             continue
         xs = [W.group(numels, "grad", W.CFG_SWEEP, 0, k, W.GRAD) for k in range(p)]
-        for oneshot in (TWOSHOT, ONESHOT, LL):
+        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL)):
             if oneshot == LL and total > (64 << 10):
                 continue
             comm = _comm(p, oneshot)
             flats = [torch.from_numpy(np.concatenate(x)).cuda() for x in xs]
             views = [list(torch.split(f, numels)) for f in flats]
-            grp = tc.Group(comm, views)
+            grp = tc.Group(comm, views if p > 1 else views[0])
             tc.allreduce(grp, 0.5)
             want = O.allreduce(xs, 0.5)
             for r in range(p):

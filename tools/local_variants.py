@@ -53,7 +53,7 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         one()
     else:
-        for v in range(5):
+        for v in range(6):
             r = subprocess.run([sys.executable, __file__, "one"], capture_output=True, text=True,
                                env=dict(os.environ, TC_VARIANT=str(v)))
             print(f"variant {v}: {r.stdout.strip()} {r.stderr.strip()[-300:]}", flush=True)

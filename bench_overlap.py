@@ -4,9 +4,15 @@
     torchrun --nproc-per-node N bench_overlap.py [--ratio 1.0] [--bucket-mb 25]
 
 PAPER.md:59: gradients "are obtained as soon as a backward step for a layer is computed, these
-can be aggregated in parallel with the backward phase".  The backward pass is synthetic: for each
-ResNet-50 tensor, last to first, a bf16 GEMM burst sized so the whole pass takes `ratio` x the
-time of one whole-group tc_sgd_step, then the tensor's gradient is written.  Three runs:
+can be aggregated in parallel with the backward phase".  The backward pass is synthetic: bucket by
+bucket, last layers first, a compute burst sized so the whole pass takes `ratio` x the time of one
+whole-group tc_sgd_step, then the bucket's gradients are written.  The burst is either
+  --compute burn: a compute-bound FMA kernel of many small CTAs (4 x 256 threads per SM, no
+                  shared memory), compiled with NVRTC -- the SURVEY's "synthetic compute kernel";
+  --compute gemm: cuBLAS bf16 GEMMs.  These are persistent kernels that want every SM: while the
+                  collective holds some SMs the GEMM's remaining CTAs start only when it ends, so
+                  the two serialise instead of overlapping (reported as measured).
+Three runs:
   compute  -- the backward pass alone;
   serial   -- backward, then one tc_sgd_step over the whole group;
   overlap  -- tc.BucketedStep: each bucket's tc_sgd_step on a side stream once its last gradient
@@ -47,9 +53,61 @@ def timed(fn, iters, world):
     return float(t) * 1e3
 
 
+BURN_SRC = r"""
+extern "C" __global__ void burn(float* out, int iters) {
+  float a = threadIdx.x * 1e-3f, b = 1.0001f, c = 0.9999f;
+  for (int i = 0; i < iters; ++i) {
+    a = a * b + c;
+    b = b * c - a * 1e-9f;
+  }
+  if (a == 12345.f) out[0] = b;
+}
+"""
+
+
+class Burn:
+    """A compute-bound kernel (FMA chains) launched on torch's current stream via NVRTC."""
+
+    def __init__(self, device):
+        from cuda.bindings import driver as cu, nvrtc
+        self.cu = cu
+        major, minor = torch.cuda.get_device_capability(device)
+        err, prog = nvrtc.nvrtcCreateProgram(BURN_SRC.encode(), b"burn.cu", 0, [], [])
+        opts = [f"--gpu-architecture=sm_{major}{minor}{'a' if major >= 9 else ''}".encode()]
+        (err,) = nvrtc.nvrtcCompileProgram(prog, len(opts), opts)
+        if err != nvrtc.nvrtcResult.NVRTC_SUCCESS:
+            _, n = nvrtc.nvrtcGetProgramLogSize(prog)
+            log = b" " * n
+            nvrtc.nvrtcGetProgramLog(prog, log)
+            raise RuntimeError(log.decode())
+        _, n = nvrtc.nvrtcGetCUBINSize(prog)
+        cubin = b" " * n
+        nvrtc.nvrtcGetCUBIN(prog, cubin)
+        cu.cuInit(0)
+        torch.cuda.synchronize()
+        err, self.mod = cu.cuModuleLoadData(cubin)
+        assert err == cu.CUresult.CUDA_SUCCESS, err
+        err, self.fn = cu.cuModuleGetFunction(self.mod, b"burn")
+        assert err == cu.CUresult.CUDA_SUCCESS, err
+        self.out = torch.zeros(1, device="cuda")
+        self.grid = 4 * torch.cuda.get_device_properties(device).multi_processor_count
+
+    def __call__(self, iters):
+        import ctypes
+        cu = self.cu
+        a0 = ctypes.c_void_p(self.out.data_ptr())
+        a1 = ctypes.c_int(int(iters))
+        args = (ctypes.c_void_p * 2)(ctypes.addressof(a0), ctypes.addressof(a1))
+        st = torch.cuda.current_stream().cuda_stream
+        (err,) = cu.cuLaunchKernel(self.fn, self.grid, 1, 1, 256, 1, 1, 0, st,
+                                   ctypes.addressof(args), 0)
+        assert err == cu.CUresult.CUDA_SUCCESS, err
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ratio", type=float, default=1.0)
+    ap.add_argument("--compute", default="burn", choices=["burn", "gemm"])
     ap.add_argument("--bucket-mb", type=float, default=25.0)
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
@@ -80,24 +138,41 @@ def main():
     comm.set_tuning(0, 0, -1)
     t_step = timed(lambda: (g_flat.copy_(gp_flat), whole_step()), a.iters, world) - \
         timed(lambda: g_flat.copy_(gp_flat), a.iters, world)
-    A = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
-    B = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
-    C = torch.empty_like(A)
-    t_gemm = timed(lambda: torch.mm(A, B, out=C), 50, world)
-    total_gemms = max(1, int(round(a.ratio * t_step / t_gemm)))
-    # The synthetic backward works bucket by bucket (few launches, so the host is not the
-    # bottleneck): a GEMM burst proportional to the bucket's bytes, then one copy writing the
-    # bucket's gradients (contiguous views of the flat gradient buffer), last layers first.
     bucket_of, nb = tc.Plan(numels).buckets(int(a.bucket_mb * (1 << 20)))
     members = [[t for t in range(len(numels)) if bucket_of[t] == k] for k in range(nb)]
     offs = np.concatenate([[0], np.cumsum(numels)])
     spans = [(int(offs[m[0]]), int(offs[m[-1] + 1])) for m in members]
-    per = [max(1, int(round(total_gemms * (hi - lo) / N))) for lo, hi in spans]
+    if a.compute == "gemm":
+        # cuBLASLt honours the SM carveout (torch._C._set_sm_carveout_experimental)
+        torch.backends.cuda.preferred_blas_library("cublaslt")
+        A = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
+        B = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
+        C = torch.empty_like(A)
+        t_unit = timed(lambda: torch.mm(A, B, out=C), 50, world)
+        total = max(1, int(round(a.ratio * t_step / t_unit)))
+        per = [max(1, int(round(total * (hi - lo) / N))) for lo, hi in spans]
+
+        def burst(k):
+            for _ in range(per[k]):
+                torch.mm(A, B, out=C)
+        units = sum(per)
+    else:
+        burn = Burn(local)
+        t_unit = timed(lambda: burn(10000), 20, world) / 10000  # us per iteration
+        total = a.ratio * t_step / t_unit
+        per = [max(100, int(round(total * (hi - lo) / N))) for lo, hi in spans]
+
+        def burst(k):
+            burn(per[k])
+        units = sum(per)
+
+    # The synthetic backward works bucket by bucket (few launches, so the host is not the
+    # bottleneck): a compute burst proportional to the bucket's bytes, then one copy writing the
+    # bucket's gradients (contiguous views of the flat gradient buffer), last layers first.
 
     def backward(after=None):
         for k in range(nb):
-            for _ in range(per[k]):
-                torch.mm(A, B, out=C)
+            burst(k)
             lo, hi = spans[k]
             g_flat[lo:hi].copy_(gp_flat[lo:hi])
             if after:
@@ -107,19 +182,27 @@ def main():
     t_compute = timed(backward, a.iters, world)
     t_serial = timed(lambda: (backward(), whole_step()), a.iters, world)
     rows = []
-    for ctas in (0, 148, 64, 32):
+    for ctas in (0, 64, 32, 16):
         step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas)
+        # GEMM mode: cuBLAS leaves `ctas` SMs to the collective (SM carveout), as a framework
+        # overlapping communication with persistent GEMMs does
+        carve = ctas if (a.compute == "gemm" and ctas) else None
+        torch._C._set_sm_carveout_experimental(carve)
 
         def overlapped():
             backward(lambda t: step.grad_ready(t, **hp))
             step.finish()
 
+        t_comp_c = timed(backward, a.iters, world) if carve else t_compute
         t_over = timed(overlapped, a.iters, world)
+        torch._C._set_sm_carveout_experimental(None)
         comm.set_tuning(0, 0, -1)
         rows.append({"bench": "overlap (NEXT row f1)", "n_gpus": world, "ctas": ctas or "auto",
                      "buckets": step.nbuckets, "bucket_mb": a.bucket_mb,
-                     "ratio": a.ratio, "gemms": sum(per),
-                     "t_step_us": t_step, "t_compute_us": t_compute, "t_serial_us": t_serial,
+                     "ratio": a.ratio, "compute": a.compute, "compute_units": units,
+                     "sm_carveout": carve,
+                     "t_step_us": t_step, "t_compute_us": t_compute,
+                     "t_compute_carveout_us": t_comp_c, "t_serial_us": t_serial,
                      "t_overlap_us": t_over,
                      "hidden_fraction": (t_serial - t_over) / max(t_serial - t_compute, 1e-9),
                      "speedup_vs_serial": t_serial / t_over})

@@ -149,8 +149,12 @@ TC_API tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes);
  * multimem.st; only for groups in tc_mem_alloc memory, else two-shot).  1 and 3 end with the
  * staged pull allgather and give bit-identical results (float64, rank order).  NVLS sums in
  * the switch in fp32 (order unspecified): exact for integer-valued data, else within
- * (p-1) ulp-scale of the float64 sum; identical on every rank.  Automatic: pull, except
- * tc_allreduce of eligible groups at p >= 6 -> NVLS.  Errors: TC_ERR_INVALID_ARG. */
+ * (p-1) ulp-scale of the float64 sum; identical on every rank.  6 = two-shot pull with the
+ * data moved by TMA bulk copies through a shared-memory stage ring (one CTA per SM at most;
+ * tc_comm_set_tuning's num_ctas sets how many SMs it occupies -- few CTAs still move data at
+ * link speed, leaving the rest of the GPU to concurrent work); bit-identical to 1 and 3.
+ * Automatic: pull, except tc_allreduce of eligible groups at p >= 6 -> NVLS.
+ * Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 
 /* Device-barrier timeout in milliseconds (default 30000, or env TC_TIMEOUT_MS). */
@@ -248,7 +252,7 @@ TC_API tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, voi
 
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
  * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS,
- * 5 = low-latency), grid CTAs per rank, threads. */
+ * 5 = low-latency, 6 = two-shot TMA), grid CTAs per rank, threads per CTA. */
 TC_API tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads);
 
 #ifdef __cplusplus

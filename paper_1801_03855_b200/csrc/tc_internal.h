@@ -33,6 +33,38 @@ constexpr int kTmaStages = 4;
 constexpr int kTmaConsumerWarps = 8;
 constexpr int kTmaThreads = 32 * (1 + kTmaConsumerWarps);
 constexpr int kTmaSmem = kTmaStages * 3 * kTileE * 4;
+// Two-shot, TMA-staged (k_twoshot_tma): owner-chunk tiles of <= kT2Slots slots inside one
+// tensor; each stage holds every operand of one tile; as many stages as fit kT2SmemCap.
+#ifndef TC_T2_SLOTS
+#define TC_T2_SLOTS 512
+#endif
+#ifndef TC_T2_SMEM
+#define TC_T2_SMEM (192 * 1024)
+#endif
+constexpr int kT2Slots = TC_T2_SLOTS;
+constexpr int kT2SmemCap = TC_T2_SMEM;
+constexpr int kT2MaxStages = 16;
+#ifndef TC_T2_CW
+#define TC_T2_CW 8
+#endif
+#ifndef TC_T2_U
+#define TC_T2_U 1
+#endif
+constexpr int kT2ConsumerWarps = TC_T2_CW;
+constexpr int kT2Unroll = TC_T2_U;
+constexpr int kT2Threads = 32 * (1 + kT2ConsumerWarps);
+// operands per stage: reduce-scatter p sources (+ w, dw for SGD; + center for EASGD);
+// allgather the staged value (+ w, dw for SGD; + x, center for EASGD)
+constexpr int t2_ops(int op, int p) {
+  const int rs = p + (op == 1 ? 2 : op == 2 ? 1 : 0);
+  const int ag = 1 + (op == 0 ? 0 : 2);
+  return rs > ag ? rs : ag;
+}
+constexpr int t2_stages(int op, int p) {
+  const int n = kT2SmemCap / (t2_ops(op, p) * kT2Slots * 16);
+  return n > kT2MaxStages ? kT2MaxStages : n;
+}
+constexpr int t2_smem(int op, int p) { return t2_stages(op, p) * t2_ops(op, p) * kT2Slots * 16; }
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
@@ -42,7 +74,8 @@ enum Algo {
   ALGO_ONESHOT = 2,
   ALGO_TWOSHOT_PUSH = 3,
   ALGO_NVLS = 4,
-  ALGO_LL = 5
+  ALGO_LL = 5,
+  ALGO_TWOSHOT_TMA = 6
 };
 
 // ---------------------------------------------------------------- A1 descriptor (host)
@@ -109,6 +142,8 @@ struct KParams {
   unsigned long long* prof; // optional per-CTA phase timestamps [nlocal*ctas][8] (ns)
   const int4* tiles;     // p = 1 TMA stream: {tensor, first element, elements, 0} per tile
   int ntiles;
+  const int4* tiles2;    // p >= 2 TMA two-shot: {tensor, first slot, slots, 0} per tile,
+  int tile2_off[kMaxRanks + 1];  // owner q's tiles: [tile2_off[q], tile2_off[q + 1])
 };
 
 // Kernel launchers (tc_kernels.cu).
@@ -116,6 +151,7 @@ struct KParams {
 cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int threads, int nlocal,
                        bool cooperative, cudaStream_t stream, int variant);
 int max_ctas_per_sm(int op, int algo, int p, int threads, int variant);
+int launch_threads(int op, int algo, int p, int threads, int variant);
 
 // ---------------------------------------------------------------- runtime objects
 // One symmetric allocation (tc_mem_alloc): every rank's physical memory mapped locally (uc[r]),
@@ -190,6 +226,8 @@ struct Group {
   float** d_mc = nullptr;
   int4* d_tiles = nullptr;       // p = 1: tile table of the TMA stream (k_local_tma)
   int ntiles = 0;
+  int4* d_tiles2 = nullptr;      // p >= 2: owner-chunk tiles of the TMA two-shot
+  std::vector<int> tile2_off;    // [p + 1]
 };
 
 }  // namespace tc

@@ -17,39 +17,50 @@ const void* select_kernel(int op, int algo, int p, int variant) {
   return nullptr;
 }
 
-// The p = 1 TMA stream (variant 0 of ALGO_LOCAL) runs kTmaThreads threads with kTmaSmem bytes
-// of dynamic shared memory.
-bool is_tma(int algo, int variant) { return algo == ALGO_LOCAL && variant == 0; }
+// TMA kernels run fixed thread counts with dynamic shared memory: the p = 1 stream (variant 0
+// of ALGO_LOCAL) and the TMA two-shot.
+struct Shape {
+  int threads;
+  int smem;
+};
+Shape shape_of(int op, int algo, int p, int threads, int variant) {
+  if (algo == ALGO_LOCAL && variant == 0) return {kTmaThreads, kTmaSmem};
+  if (algo == ALGO_TWOSHOT_TMA) return {kT2Threads, t2_smem(op, p)};
+  return {threads, 0};
+}
 
-cudaError_t prepare(const void* k, int algo, int variant) {
-  if (!is_tma(algo, variant)) return cudaSuccess;
-  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+cudaError_t prepare(const void* k, const Shape& sh) {
+  if (sh.smem == 0) return cudaSuccess;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem);
 }
 
 }  // namespace
 
 int max_ctas_per_sm(int op, int algo, int p, int threads, int variant) {
   const void* k = select_kernel(op, algo, p, variant);
-  if (!k || prepare(k, algo, variant) != cudaSuccess) return 0;
+  const Shape sh = shape_of(op, algo, p, threads, variant);
+  if (!k || prepare(k, sh) != cudaSuccess) return 0;
   int n = 0;
-  const bool tma = is_tma(algo, variant);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, tma ? kTmaThreads : threads,
-                                                    tma ? kTmaSmem : 0) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, sh.threads, sh.smem) != cudaSuccess)
     return 0;
   return n;
+}
+
+int launch_threads(int op, int algo, int p, int threads, int variant) {
+  return shape_of(op, algo, p, threads, variant).threads;
 }
 
 cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int threads, int nlocal,
                        bool cooperative, cudaStream_t stream, int variant) {
   const void* k = select_kernel(op, algo, kp.p, variant);
   if (!k) return cudaErrorInvalidValue;
-  cudaError_t e = prepare(k, algo, variant);
+  const Shape sh = shape_of(op, algo, kp.p, threads, variant);
+  cudaError_t e = prepare(k, sh);
   if (e != cudaSuccess) return e;
   KParams arg = kp;
   void* args[] = {&arg};
-  const bool tma = is_tma(algo, variant);
-  dim3 grid(ctas, nlocal), block(tma ? kTmaThreads : threads);
-  const size_t smem = tma ? kTmaSmem : 0;
+  dim3 grid(ctas, nlocal), block(sh.threads);
+  const size_t smem = sh.smem;
   if (cooperative) return cudaLaunchCooperativeKernel(k, grid, block, args, smem, stream);
   return cudaLaunchKernel(k, grid, block, args, smem, stream);
 }

@@ -1102,6 +1102,287 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
   }
 }
 
+// ------------------------------------------------------------------ two-shot, TMA-staged
+// The pulled two-shot with its data movement on the TMA engines.  Warp 0 is the producer:
+// its 32 lanes fetch the descriptors of 32 tiles at once (one latency for 32 table walks),
+// then issue cp.async.bulk copies of each tile's operands -- the p ranks' tensors in the
+// reduce-scatter, the owner's staged chunk in the allgather, plus the local epilogue operands --
+// into a ring of shared-memory stages, a stage holding G tiles when a phase has fewer operands
+// than the stage has room for.  8 consumer warps reduce (float64, rank order), apply the
+// epilogue and store.  Bytes in flight per CTA = the ring (up to 160 KiB), not one register
+// load per thread, so a few CTAs drive the links and the other SMs stay free for computation
+// running beside the collective (NEXT row f1).  Same tiles-to-CTA pairing (tile i of a chunk ->
+// CTA i mod grid on every rank), staging, barriers and arithmetic as k_twoshot_pull.
+struct T2Desc {
+  float* a;     // this rank's tensors at the tile's first element
+  float* b;
+  float* c;
+  float* st;    // staging at the tile's first slot: my chunk (RS) or the owner's (AG)
+  int64_t e;    // element of the tile's first slot in tensor t (negative: shifted head)
+  int t, n;     // tensor, slots
+  int vec, pad; // 16-B aligned full slots in every operand: bulk path
+};
+
+__host__ __device__ constexpr int t2_pack(int x) {
+  return x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1;
+}
+
+template <int OP, int P, int PH, int G, int OPSP, int OPS, int NS>
+__device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float* stagebuf,
+                                         int& k, uint64_t* full, uint64_t* empty,
+                                         T2Desc (*desc)[8], float4* sm4,
+                                         unsigned long long& waited) {
+  using N = Needs<OP, PH, PH == PH_RS ? P : 2>;
+  constexpr int V = kT2Slots;
+  const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  const size_t T = (size_t)kp.T;
+  const int lo = (int)((int64_t)kp.M * qo / P);
+  const int first = kp.tile2_off[qo] + (int)blockIdx.x, end = kp.tile2_off[qo + 1];
+  const int cnt = first < end ? (end - first + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  auto stage = [&](int s, int o) { return sm4 + ((size_t)s * OPS + o) * V; };
+  if (warp == 0) {
+    if (lane_id == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+    for (int base = 0; base < cnt; base += 32) {
+      const int j = base + lane_id;
+      const bool valid = j < cnt;
+      T2Desc d{};
+      const float* src[OPSP];
+      uint32_t bytes = 0;
+      if (valid) {
+        const int4 tl = kp.tiles2[first + j * (int)gridDim.x];
+        d.t = tl.x;
+        d.n = tl.z;
+        d.e = (int64_t)(tl.y - kp.prefix[d.t]) * 4 - kp.shift[d.t];
+        const size_t mine = (size_t)r * T + d.t;
+        d.a = kp.a[mine] + d.e;
+        d.b = (N::loadB || N::storeB) ? kp.b[mine] + d.e : nullptr;
+        d.c = (N::loadC || N::storeC) ? kp.c[mine] + d.e : nullptr;
+        d.st = stagebuf + (size_t)(tl.y - lo) * 4;
+        bool vec = d.e >= 0 && d.e + 4 * (int64_t)d.n <= kp.numel[d.t];
+        int o = 0;
+        if constexpr (PH == PH_RS) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) src[o++] = kp.a[q * T + d.t] + d.e;
+        } else {
+          src[o++] = d.st;
+          if constexpr (N::loadA) src[o++] = d.a;
+        }
+        if constexpr (N::loadB) src[o++] = d.b;
+        if constexpr (N::loadC) src[o++] = d.c;
+#pragma unroll
+        for (int x = 0; x < OPSP; ++x) vec = vec && (((uintptr_t)src[x] & 15) == 0);
+        vec = vec && (((uintptr_t)d.a & 15) == 0);
+        d.vec = vec;
+        bytes = vec ? (uint32_t)d.n * 16 * OPSP : 0;
+      }
+      const int bc = min(32, cnt - base);
+      for (int u0 = 0; u0 < bc; u0 += G) {
+        const int s = k % NS;
+        const bool in_unit = valid && lane_id >= u0 && lane_id < u0 + G;
+        const uint32_t ub = __reduce_add_sync(0xffffffffu, in_unit ? bytes : 0u);
+        if (lane_id == u0 && k >= NS) {
+          const unsigned long long t0 = kp.prof ? globaltimer() : 0;
+          mbar_wait(&empty[s], (uint32_t)((k / NS - 1) & 1));
+          if (kp.prof) waited += globaltimer() - t0;
+        }
+        __syncwarp();
+        if (in_unit) desc[s][lane_id - u0] = d;
+        __syncwarp();
+        if (lane_id == u0) {
+          if (ub)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             smem_u32(&full[s])),
+                         "r"(ub)
+                         : "memory");
+          else
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s]))
+                         : "memory");
+        }
+        __syncwarp();
+        if (in_unit && d.vec) {
+#pragma unroll
+          for (int x = 0; x < OPSP; ++x)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                "%2, [%3];" ::"r"(smem_u32(stage(s, (lane_id - u0) * OPSP + x))),
+                "l"(src[x]), "r"((uint32_t)d.n * 16), "r"(smem_u32(&full[s]))
+                : "memory");
+        }
+        ++k;
+      }
+    }
+    return;
+  }
+  // consumers
+  const int ct = threadIdx.x - 32, nct = kT2Threads - 32;
+  for (int base = 0; base < cnt; base += 32) {
+    const int bc = min(32, cnt - base);
+    for (int u0 = 0; u0 < bc; u0 += G) {
+      const int s = k % NS;
+      const int ut = min(G, bc - u0);
+      {
+        const unsigned long long t0 = kp.prof ? globaltimer() : 0;
+        mbar_wait(&full[s], (uint32_t)((k / NS) & 1));
+        if (kp.prof) waited += globaltimer() - t0;
+      }
+      for (int jt = 0; jt < ut; ++jt) {
+        const T2Desc d = desc[s][jt];
+        if (d.vec) {
+          const float4* so = stage(s, jt * OPSP);
+          constexpr int TU = kT2Unroll;
+          for (int v0 = ct; v0 < d.n; v0 += nct * TU) {
+            if constexpr (PH == PH_RS) {
+              constexpr int NB = N::loadB ? 1 : 0;
+              float4 x[TU][P], b[TU], c[TU];
+#pragma unroll
+              for (int u = 0; u < TU; ++u) {
+                const int v = v0 + u * nct;
+                if (v < d.n) {
+#pragma unroll
+                  for (int q = 0; q < P; ++q) x[u][q] = so[q * V + v];
+                  b[u] = N::loadB ? so[P * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                  c[u] = N::loadC ? so[(P + NB) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < TU; ++u) {
+                const int v = v0 + u * nct;
+                if (v >= d.n) continue;
+                float4 oa;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                  float in[P];
+#pragma unroll
+                  for (int q = 0; q < P; ++q) in[q] = lane_of(x[u][q], l);
+                  float la = 0.f, lb = lane_of(b[u], l), lc = lane_of(c[u], l);
+                  elem<OP, PH_RS, P>(kp, r, in, la, lb, lc);
+                  lane(oa, l) = la;
+                  lane(b[u], l) = lb;
+                  lane(c[u], l) = lc;
+                }
+                if constexpr (N::storeA) st16(d.a + 4 * v, oa);
+                if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
+                if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
+                st16(d.st + 4 * v, OP == OP_EASGD ? b[u] : oa);
+              }
+            } else {
+              constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
+              float4 x[TU], a[TU], b[TU], c[TU];
+#pragma unroll
+              for (int u = 0; u < TU; ++u) {
+                const int v = v0 + u * nct;
+                if (v < d.n) {
+                  x[u] = so[v];
+                  a[u] = N::loadA ? so[OA * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                  b[u] = N::loadB ? so[OB * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                  c[u] = N::loadC ? so[OC * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < TU; ++u) {
+                const int v = v0 + u * nct;
+                if (v >= d.n) continue;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                  const float in[1] = {lane_of(x[u], l)};
+                  float la = lane_of(a[u], l), lb = lane_of(b[u], l), lc = lane_of(c[u], l);
+                  elem<OP, PH_AG, 2>(kp, r, in, la, lb, lc);
+                  lane(a[u], l) = la;
+                  lane(b[u], l) = lb;
+                  lane(c[u], l) = lc;
+                }
+                st16(d.a + 4 * v, a[u]);
+                if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
+                if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
+              }
+            }
+          }
+        } else {
+          // element path (shifted heads, partial tails, operands misaligned on some rank)
+          const int64_t j0 = d.e < 0 ? -d.e : 0;
+          const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
+          for (int64_t j = j0 + ct; j < j1; j += nct) {
+            if constexpr (PH == PH_RS) {
+              float in[P];
+#pragma unroll
+              for (int q = 0; q < P; ++q) in[q] = ld4(kp.a[q * T + d.t] + d.e + j);
+              float la = 0.f, lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
+              elem<OP, PH_RS, P>(kp, r, in, la, lb, lc);
+              if constexpr (N::storeA) st4(d.a + j, la);
+              if constexpr (N::storeB) st4(d.b + j, lb);
+              if constexpr (N::storeC) st4(d.c + j, lc);
+              st4(d.st + j, OP == OP_EASGD ? lb : la);
+            } else {
+              const float in[1] = {ld4(d.st + j)};
+              float la = N::loadA ? ld4(d.a + j) : 0.f;
+              float lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
+              elem<OP, PH_AG, 2>(kp, r, in, la, lb, lc);
+              st4(d.a + j, la);
+              if constexpr (N::storeB) st4(d.b + j, lb);
+              if constexpr (N::storeC) st4(d.c + j, lc);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane_id == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
+                     : "memory");
+      ++k;
+    }
+  }
+}
+
+template <int OP, int P>
+__global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
+  using NR = Needs<OP, PH_RS, P>;
+  using NG = Needs<OP, PH_AG, 2>;
+  constexpr int OPS = t2_ops(OP, P), NS = t2_stages(OP, P);
+  constexpr int OPS_RS = P + NR::loadB + NR::loadC;
+  constexpr int OPS_AG = 1 + NG::loadA + NG::loadB + NG::loadC;
+  constexpr int G_RS = t2_pack(OPS / OPS_RS), G_AG = t2_pack(OPS / OPS_AG);
+  static_assert(OPS_RS <= OPS && OPS_AG <= OPS, "stage too small");
+  extern __shared__ __align__(128) float4 sm4[];  // [NS][OPS][kT2Slots]
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  __shared__ T2Desc desc[NS][8];
+  const int r = kp.rank0 + (int)blockIdx.y;
+  if (r == kp.absent_rank) return;
+  call_begin(kp, r);
+  const int par = (int)(ep() & 1u);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[s])),
+                   "r"(kT2ConsumerWarps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  stamp(kp, 0);
+  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
+  stamp(kp, 1);
+  int k = 0;  // position in the stage ring (continues across phases)
+  unsigned long long waited = 0;  // profiling: producer waits for empty / consumers for full
+  t2_phase<OP, P, PH_RS, G_RS, OPS_RS, OPS, NS>(kp, r, r, arena_stage(kp, r, par), k, full,
+                                                 empty, desc, sm4, waited);
+  stamp(kp, 2);
+  if (!barrier_all(kp, r, BAR_MID, true)) return;
+  stamp(kp, 3);
+#pragma unroll 1
+  for (int jq = 0; jq < P - 1; ++jq) {
+    const int qo = (r + 1 + jq) % P;
+    t2_phase<OP, P, PH_AG, G_AG, OPS_AG, OPS, NS>(kp, r, qo, arena_stage(kp, qo, par), k, full,
+                                                   empty, desc, sm4, waited);
+  }
+  stamp(kp, 4);
+  if (kp.prof != nullptr && threadIdx.x < 32)  // producer lanes each timed their own waits
+    for (int o = 16; o > 0; o >>= 1) waited += __shfl_xor_sync(0xffffffffu, waited, o);
+  if (kp.prof != nullptr && (threadIdx.x == 0 || threadIdx.x == 32))
+    kp.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (threadIdx.x ? 7 : 6)] = waited;
+  call_end(kp, r);
+  stamp(kp, 5);
+}
+
 template <int OP>
 const void* kernel_ptr(int algo, int p, int variant) {
   if (algo == ALGO_LOCAL) {
@@ -1122,6 +1403,7 @@ const void* kernel_ptr(int algo, int p, int variant) {
       if (algo == ALGO_NVLS)                                                         \
         return variant == 1 ? (const void*)k_nvls<OP, PP, 1> : (const void*)k_nvls<OP, PP, 2>; \
     if (algo == ALGO_NVLS) return nullptr;                                           \
+    if (algo == ALGO_TWOSHOT_TMA) return (const void*)k_twoshot_tma<OP, PP>;         \
     if (algo == ALGO_LL)                                                             \
       return variant == 1 ? (const void*)k_ll<OP, PP, 1> : (const void*)k_ll<OP, PP, 2>; \
     if (variant == 1)                                                                \

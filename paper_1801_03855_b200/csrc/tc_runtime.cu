@@ -153,6 +153,9 @@ void free_group_device(Group& g) {
   cudaFree(g.d_tiles);
   g.d_tiles = nullptr;
   g.ntiles = 0;
+  cudaFree(g.d_tiles2);
+  g.d_tiles2 = nullptr;
+  g.tile2_off.clear();
   g.d_ptrs = nullptr;
   g.d_prefix = nullptr;
   g.d_block_t = nullptr;
@@ -223,6 +226,41 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
     if (g.ntiles) {
       TC_CUDA(cudaMalloc((void**)&g.d_tiles, sizeof(int4) * tiles.size()));
       TC_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(int4) * tiles.size(),
+                         cudaMemcpyHostToDevice));
+    }
+  }
+  if (g.comm->nranks > 1) {
+    // TMA two-shot: each owner chunk [M q / p, M (q+1) / p) of the device grid cut into tiles
+    // of <= kT2Slots slots inside one tensor.  A shifted tensor's partial first slot and a
+    // partial last slot are one-slot tiles of their own (element path in the kernel).
+    const int p = g.comm->nranks;
+    std::vector<int4> tiles;
+    g.tile2_off.assign((size_t)p + 1, 0);
+    int t = 0;
+    for (int q = 0; q < p; ++q) {
+      g.tile2_off[(size_t)q] = (int)tiles.size();
+      const int64_t lo = g.M * q / p, hi = g.M * (q + 1) / p;
+      while (t < pl.T && g.dev_prefix[(size_t)t + 1] <= lo) ++t;
+      for (int u = t; u < pl.T && g.dev_prefix[(size_t)u] < hi; ++u) {
+        const int64_t pre = g.dev_prefix[(size_t)u], end = g.dev_prefix[(size_t)u + 1];
+        int64_t a = std::max(lo, pre);
+        const int64_t b = std::min(hi, end);
+        if (a >= b) continue;
+        const int64_t m = g.shift[(size_t)u], n = pl.numel[(size_t)u];
+        const int64_t first_full = pre + (m ? 1 : 0);
+        const int64_t full_end = end - (((n + m) & 3) ? 1 : 0);
+        if (a < first_full) tiles.push_back(make_int4(u, (int)a++, 1, 0));
+        const int64_t vend = std::min(b, full_end);
+        for (int64_t x = a; x < vend; x += kT2Slots)
+          tiles.push_back(make_int4(u, (int)x, (int)std::min<int64_t>(kT2Slots, vend - x), 0));
+        const int64_t rest = std::max(a, vend);
+        if (b > rest) tiles.push_back(make_int4(u, (int)rest, (int)(b - rest), 0));
+      }
+    }
+    g.tile2_off[(size_t)p] = (int)tiles.size();
+    if (!tiles.empty()) {
+      TC_CUDA(cudaMalloc((void**)&g.d_tiles2, sizeof(int4) * tiles.size()));
+      TC_CUDA(cudaMemcpy(g.d_tiles2, tiles.data(), sizeof(int4) * tiles.size(),
                          cudaMemcpyHostToDevice));
     }
   }
@@ -341,15 +379,18 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     algo = ALGO_LOCAL;
   } else {
     // One-shot moves (p-1)S per GPU against 2(p-1)/p S for two-shot but needs one barrier
-    // instead of a chain of per-owner waits: measured to win up to the 8 MiB staging capacity at
-    // p <= 4 (p = 4, 4 MiB: 34 us vs 52 two-shot, NCCL 35).
-    const int64_t auto_lim = p <= 4 ? (int64_t)kStageCapacity : kDefaultOneshotMax;
+    // less.  Measured crossover against the TMA two-shot (config-5 sweep): p = 2 one-shot
+    // 22-23 us at 4 MiB (TMA 24-35), two-shot from 16 MiB; p = 4 even at 4 MiB (34-36 vs 29-37
+    // us), TMA ahead above.
+    const int64_t auto_lim = p == 2 ? (int64_t)kStageCapacity
+                           : p <= 4 ? (int64_t)kStageCapacity / 2 : kDefaultOneshotMax;
     int64_t lim = c.tune_oneshot < 0 ? auto_lim : c.tune_oneshot;
     if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
     // Automatic choice (measured on B200, config-5 sweep and ResNet-50 group):
-    // pulled two-shot up to p = 5 (p = 4: 16/64/256 MiB in 72/189/679 us vs 95/210/737 pushed,
-    // NCCL 70/185/685); p >= 6 -> NVLS when the group is multicast-bound (it moves (1 + 1/p) S
-    // per GPU instead of 2(p-1)/p S, 1.56x less at p = 8), else pulled.
+    // TMA-staged two-shot (p = 4: 16/64/256 MiB in 58-67/176-184/635-650 us; LDG pull
+    // 72/189/679, pushed 95/210/737, NCCL 70/186/685); p >= 6 -> NVLS for the allreduce of a
+    // multicast-bound group (it moves (1 + 1/p) S per GPU instead of 2(p-1)/p S, 1.56x less at
+    // p = 8; not measured on 8 GPUs here), else the TMA two-shot.
     const bool nvls_ok = ga->d_mc != nullptr && op != OP_EASGD;
     // Low-latency (LL): every element travels once to every peer as an 8-byte {value, epoch}
     // word and is awaited in local memory -- no barrier round trip (small groups only).
@@ -363,13 +404,17 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
     else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;
     else if (c.algo_override == ALGO_TWOSHOT_PUSH) algo = ALGO_TWOSHOT_PUSH;
+    else if (c.algo_override == ALGO_TWOSHOT_TMA) algo = ALGO_TWOSHOT_TMA;
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
     // (automatic NVLS only for the plain allreduce: the fused SGD step's HBM epilogue cannot
     // start before the switch has reduced a chunk, measured 405 us vs 297 us pulled at p = 4)
     else if (nvls_ok && (c.algo_override == ALGO_NVLS || (p >= 6 && op == OP_ALLREDUCE)))
       algo = ALGO_NVLS;
-    else algo = ALGO_TWOSHOT;
-    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH) && (Mdev + p - 1) / p + 1 > c.arena_cap)
+    // TMA-staged two-shot: ResNet-50 group p = 2 allreduce 188 / SGD step 197 us (LDG pull
+    // 208 / 226, NCCL allreduce 219); p = 4 262 / 278 us (pull 289 / 301, NCCL 274-276).
+    else algo = ALGO_TWOSHOT_TMA;
+    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH || algo == ALGO_TWOSHOT_TMA) &&
+        (Mdev + p - 1) / p + 1 > c.arena_cap)
       return TC_ERR_CUDA;
   }
   const int nlocal = c.emulated ? p : 1;
@@ -381,7 +426,14 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   int64_t work_slots = twoshot ? (Mdev + p - 1) / p : Mdev;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
-  if (algo == ALGO_LOCAL && c.variant == 0) {  // TMA stream
+  if (algo == ALGO_TWOSHOT_TMA) {
+    // bytes in flight come from the stage ring, not from threads: one CTA per SM at most
+    const int tiles_r = ga->tile2_off[1] - ga->tile2_off[0];
+    ctas = c.tune_ctas > 0 ? c.tune_ctas : c.num_sms;
+    ctas = std::max(1, std::min(ctas, std::max(tiles_r, 1)));
+    kp.tiles2 = ga->d_tiles2;
+    for (int q = 0; q <= p; ++q) kp.tile2_off[q] = ga->tile2_off[(size_t)q];
+  } else if (algo == ALGO_LOCAL && c.variant == 0) {  // TMA stream
     ctas = std::min(ga->ntiles, c.tune_ctas > 0 ? std::min(c.tune_ctas, c.num_sms * occ)
                                                 : c.num_sms * occ);
     kp.tiles = ga->d_tiles;
@@ -410,7 +462,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   }
   c.last_algo = algo;
   c.last_ctas = ctas;
-  c.last_threads = (algo == ALGO_LOCAL && c.variant == 0) ? kTmaThreads : threads;
+  c.last_threads = launch_threads(op, algo, p, threads, c.variant);
   return TC_OK;
 }
 
@@ -544,7 +596,8 @@ tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes) {
 }
 
 tc_status tc_comm_set_algorithm(tc_comm* comm, int algo) {
-  if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH && algo != ALGO_NVLS))
+  if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH &&
+                algo != ALGO_NVLS && algo != ALGO_TWOSHOT_TMA))
     return TC_ERR_INVALID_ARG;
   comm->c.algo_override = algo;
   return TC_OK;

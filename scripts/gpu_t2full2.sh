@@ -1,0 +1,3 @@
+export TC_TIMEOUT_MS=20000
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+bash scripts/gpu_overlap2.sh 2>&1 | grep -v "rc=0"

@@ -27,7 +27,9 @@ ONESHOT = 1 << 20   # force one-shot
 TWOSHOT = 0         # force two-shot (pull reduce-scatter)
 PUSH = -2           # force two-shot with pushed reduce-scatter
 LL = -3             # force the low-latency algorithm
-ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT), ("ll", LL)]
+TMA = -4            # force the TMA-staged two-shot
+ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT), ("ll", LL),
+         ("two-shot-tma", TMA)]
 
 
 def _comm(p, oneshot=-1, ctas=0):
@@ -39,6 +41,9 @@ def _comm(p, oneshot=-1, ctas=0):
         c.set_ll_max(0)
     if oneshot == PUSH:
         c.set_algorithm(3)
+        oneshot = 0
+    elif oneshot == TMA:
+        c.set_algorithm(6)
         oneshot = 0
     elif oneshot == TWOSHOT and p > 1:
         c.set_algorithm(1)
@@ -102,7 +107,7 @@ def test_unaligned_tensors(p, offset):
     numels = [7, 13, 1000, 4096, 3, 1, 2]
     xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
     off = (lambda k: k % 4) if offset == "per-rank" else offset
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot, offset=off)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -141,7 +146,7 @@ def test_fewer_slots_than_ranks(p):
     """N < p: some owners have empty chunks."""
     numels = [1, 2] if p == 4 else [3, 0, 1]
     xs = [W.group(numels, "int", 75, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH):
+    for oneshot in (TWOSHOT, PUSH, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -152,7 +157,7 @@ def test_many_tensors_1024():
     g = np.random.default_rng(5)
     numels = W.random_numels(g, 1024, 700)
     xs = [W.group(numels, "grad", 74, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -164,7 +169,7 @@ def test_cta_counts(ctas):
     p = 3
     numels = [7, 13, 1000, 50000, 9]
     xs = [W.group(numels, "grad", 73, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH):
+    for oneshot in (TWOSHOT, PUSH, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot, ctas=ctas)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -396,7 +401,8 @@ def _sampled_check(numels, outs, xs, scale, p, seed=0, per_tensor=48):
 
 
 @pytest.mark.parametrize("group,p,oneshot", [("resnet50", 1, -1), ("resnet50", 2, TWOSHOT),
-                                             ("resnet50", 4, PUSH), ("alexnet", 2, TWOSHOT)])
+                                             ("resnet50", 4, PUSH), ("alexnet", 2, TWOSHOT),
+                                             ("resnet50", 4, TMA)])
 def test_full_size_groups_sampled(group, p, oneshot):
     """Configs 2/3 at their full size (ResNet-50 25.6M, AlexNet 61.1M fp32 per rank), in the
     launch configuration bench.py times, checked on sampled outputs."""
@@ -417,7 +423,7 @@ def test_config5_sweep_shapes(p, T):
         if not numels:
             continue
         xs = [W.group(numels, "grad", W.CFG_SWEEP, 0, k, W.GRAD) for k in range(p)]
-        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL)):
+        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL, TMA)):
             if oneshot == LL and total > (64 << 10):
                 continue
             comm = _comm(p, oneshot)

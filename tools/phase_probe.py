@@ -65,6 +65,9 @@ def main():
         d = np.diff(t[:, :6], axis=1) / 1e3
         span = (t[:, 5].max() - t[:, 0].min()) / 1e3
         line = " ".join(f"{n}={np.median(d[:, i]):7.1f}/{d[:, i].max():7.1f}" for i, n in enumerate(names))
+        if a.algo == 6:  # TMA two-shot: producer waiting for free stages / consumers for data
+            line += (f" | wait_empty={np.median(t[:, 6]) / 1e3:7.1f}"
+                     f" wait_full={np.median(t[:, 7]) / 1e3:7.1f}")
         msg = (f"rank {rank} algo{a.algo} {op:9s} ctas={ctas} thr={thr} span={span:7.1f}us "
                f"(busbw@span {S * 2 * (p - 1) / p / span / 1e3:6.1f} GB/s) | med/max us: {line}")
         for r in range(p):

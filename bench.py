@@ -394,6 +394,39 @@ def main():
                           "nvlink_ingress_gbs": (c - 1) * S / te / 1e9 if c > 1 else 0.0,
                           "hbm_gbs_local": 4 * S / te / 1e9 if c == 1 else None,
                           "algo": ecomm.last_launch()[0]}
+        # NEXT row f2: the same update fused with each client's own SGD step (tc_esgd_step),
+        # against the separate calls (tc_easgd_update + a local tc_sgd_step)
+        _, g_c = dev(W.group(numels, "grad", W.CFG_EASGD, 1, rank, W.GRAD))
+        _, d_c = dev(W.group(numels, "dw", W.CFG_EASGD, 2, rank, W.DW))
+        Gc, Dc = tc.Group(ecomm, g_c), tc.Group(ecomm, d_c)
+        lcomm = comm if p == 1 else tc.Comm.single(local)
+        Wl, Gl, Dl = tc.Group(lcomm, x_c), tc.Group(lcomm, g_c), tc.Group(lcomm, d_c)
+        ehp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 128)
+
+        def timed_calls(fn):
+            with torch.cuda.stream(stream):
+                for _ in range(args.warmup):
+                    fn()
+                barrier(world)
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                for _ in range(K):
+                    fn()
+                a1.record(stream)
+                stream.synchronize()
+            return max_over_ranks(a0.elapsed_time(a1) / K, world) * 1e3
+
+        t_fused = timed_calls(lambda: tc.esgd_step(X, C, Gc, Dc, 0.1, stream=stream, **ehp))
+        t_sep = timed_calls(lambda: (tc.easgd_update(X, C, 0.1, stream=stream),
+                                     tc.sgd_step(Wl, Gl, Dl, stream=stream, **ehp)))
+        extra["esgd_fused"] = {"t_us": t_fused, "t_separate_us": t_sep, "clients": c,
+                               "algo": ecomm.last_launch()[0],
+                               "note": "NEXT row f2: tc_esgd_step vs tc_easgd_update + local "
+                                       "tc_sgd_step, one GPU per client"}
+        for grp in (Gc, Dc, Wl, Gl, Dl):
+            grp.destroy()
+        if lcomm is not comm:
+            lcomm.destroy()
         X.destroy()
         C.destroy()
         if ecomm is not comm:

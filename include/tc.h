@@ -250,6 +250,22 @@ TC_API tc_status tc_sgd_step(tc_group* w, tc_group* g, tc_group* dw, float lr, f
  * TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_TIMEOUT, TC_ERR_BUSY, TC_ERR_CUDA. */
 TC_API tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream);
 
+/* NEXT row f2: the elastic update of tc_easgd_update followed, in the same
+ * pass over memory, by the SGD-momentum update of tc_sgd_step applied to the elastically moved
+ * parameters with THIS rank's own gradient (not reduced: one GPU per client, as in config 1's
+ * "4 workers" or Fig. code-snippet-4 at one GPU per worker; the paper's order is Elastic2 then
+ * SGD.Update in the same iteration).  Per element, fp32 with every op rounded:
+ *     d   = x - xc;                xe  = x - alpha*d
+ *     xc := xc + alpha*(d_0 + ... + d_{c-1})          (client order)
+ *     t   = rescale*g + wd*xe;     dw := momentum*dw - lr*t;     x := xe + dw
+ * x, center, g, dw: congruent groups on one comm (one rank per client); g is read only.
+ * One kernel: the TMA two-shot (p >= 2) or the TMA stream (p = 1).  Reads x, xc, g, dw once and
+ * writes x, xc, dw once (8S of HBM per GPU instead of 10S for tc_easgd_update + a local
+ * tc_sgd_step), NVLink traffic as tc_easgd_update.  Errors: as tc_sgd_step; alpha in [0, 1]. */
+TC_API tc_status tc_esgd_step(tc_group* x, tc_group* center, tc_group* g, tc_group* dw,
+                              float alpha, float lr, float momentum, float wd, float rescale,
+                              void* stream);
+
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
  * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS,
  * 5 = low-latency, 6 = two-shot TMA), grid CTAs per rank, threads per CTA. */

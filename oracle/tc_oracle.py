@@ -233,6 +233,24 @@ def easgd_update_f64(xs, center, alpha):
 
 
 # ----------------------------------------------------------------------------------------
+# NEXT row f2: elastic averaging then SGD in the same iteration, one GPU per client
+# (Fig. code-snippet-4: Elastic2 before SGD.Update; reading R10 for the center).
+# ----------------------------------------------------------------------------------------
+def esgd_step(xs, center, gs, dws, alpha, lr, momentum, wd, rescale):
+    """Client i (one rank) holds params xs[i], momentum dws[i] and its own gradient gs[i]; the
+    center is replicated.  easgd_update across the clients, then every client's sgd_step with
+    its own (unreduced) gradient applied to its elastically moved params.  Returns
+    ([x_i''], xc', [dw_i'])."""
+    x_el, c_new = easgd_update(xs, center, alpha)
+    x_out, dw_out = [], []
+    for i in range(len(xs)):
+        _, w_new, dw_new = sgd_step([x_el[i]], [gs[i]], [dws[i]], lr, momentum, wd, rescale)
+        x_out.append(w_new[0])
+        dw_out.append(dw_new[0])
+    return x_out, c_new, dw_out
+
+
+# ----------------------------------------------------------------------------------------
 # Config 4: MPI Elastic SGD loop (Fig. code-snippet-4, P:301-315; reading R9/R10/R11).
 # ----------------------------------------------------------------------------------------
 def esgd_sequence(x0, center0, dw0, grads, steps, tau, alpha, lr, momentum, wd, rescale):

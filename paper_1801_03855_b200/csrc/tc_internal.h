@@ -32,7 +32,8 @@ constexpr int kTileE = 2048;
 constexpr int kTmaStages = 4;
 constexpr int kTmaConsumerWarps = 8;
 constexpr int kTmaThreads = 32 * (1 + kTmaConsumerWarps);
-constexpr int kTmaSmem = kTmaStages * 3 * kTileE * 4;
+constexpr int kTmaSmem = kTmaStages * 3 * kTileE * 4;      // three operands (SGD: g, w, dw)
+constexpr int kTmaSmem4 = kTmaStages * 4 * kTileE * 4;     // four (ESGD: x, center, dw, g)
 // Two-shot, TMA-staged (k_twoshot_tma): owner-chunk tiles of <= kT2Slots slots inside one
 // tensor; each stage holds every operand of one tile; as many stages as fit kT2SmemCap.
 #ifndef TC_T2_SLOTS
@@ -55,9 +56,10 @@ constexpr int kT2Unroll = TC_T2_U;
 constexpr int kT2Threads = 32 * (1 + kT2ConsumerWarps);
 // operands per stage: reduce-scatter p sources (+ w, dw for SGD; + center for EASGD);
 // allgather the staged value (+ w, dw for SGD; + x, center for EASGD)
+// (ESGD, NEXT row f2: + w (= x), center, dw and the local gradient g)
 constexpr int t2_ops(int op, int p) {
-  const int rs = p + (op == 1 ? 2 : op == 2 ? 1 : 0);
-  const int ag = 1 + (op == 0 ? 0 : 2);
+  const int rs = p + (op == 1 ? 2 : op == 2 ? 1 : op == 3 ? 3 : 0);
+  const int ag = 1 + (op == 0 ? 0 : op == 3 ? 4 : 2);
   return rs > ag ? rs : ag;
 }
 constexpr int t2_stages(int op, int p) {
@@ -67,7 +69,7 @@ constexpr int t2_stages(int op, int p) {
 constexpr int t2_smem(int op, int p) { return t2_stages(op, p) * t2_ops(op, p) * kT2Slots * 16; }
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
-enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2 };
+enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3 };
 enum Algo {
   ALGO_LOCAL = 0,
   ALGO_TWOSHOT = 1,
@@ -127,7 +129,8 @@ struct KParams {
   const uint8_t* shift_c;
   float* const* a;       // [p*T] primary group: x (allreduce, easgd) or g (sgd)
   float* const* b;       // [p*T] w (sgd) or center (easgd)
-  float* const* c;       // [p*T] dw (sgd)
+  float* const* c;       // [p*T] dw (sgd, esgd)
+  float* const* d;       // [p*T] this rank's gradient (esgd), else nullptr
   float* const* mc;      // [T] multicast addresses of the primary group (NVLS), or nullptr
   uint32_t* const* flags;// [p] flag buffers (peer-mapped)
   float* const* stage;   // [p] one-shot staging (+ low-latency buffers), peer-mapped

@@ -6,6 +6,7 @@ namespace tc {
 const void* kernel_ptr_allreduce(int algo, int p, int variant);
 const void* kernel_ptr_sgd(int algo, int p, int variant);
 const void* kernel_ptr_easgd(int algo, int p, int variant);
+const void* kernel_ptr_esgd(int algo, int p, int variant);
 
 namespace {
 const void* select_kernel(int op, int algo, int p, int variant) {
@@ -13,6 +14,7 @@ const void* select_kernel(int op, int algo, int p, int variant) {
     case OP_ALLREDUCE: return kernel_ptr_allreduce(algo, p, variant);
     case OP_SGD: return kernel_ptr_sgd(algo, p, variant);
     case OP_EASGD: return kernel_ptr_easgd(algo, p, variant);
+    case OP_ESGD: return kernel_ptr_esgd(algo, p, variant);
   }
   return nullptr;
 }
@@ -24,7 +26,8 @@ struct Shape {
   int smem;
 };
 Shape shape_of(int op, int algo, int p, int threads, int variant) {
-  if (algo == ALGO_LOCAL && variant == 0) return {kTmaThreads, kTmaSmem};
+  if (algo == ALGO_LOCAL && variant == 0)
+    return {kTmaThreads, op == OP_ESGD ? kTmaSmem4 : kTmaSmem};
   if (algo == ALGO_TWOSHOT_TMA) return {kT2Threads, t2_smem(op, p)};
   return {threads, 0};
 }

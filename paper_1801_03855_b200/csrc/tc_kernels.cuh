@@ -166,13 +166,15 @@ enum Phase { PH_RS = 0, PH_AG = 1 };
 
 // Local operands of (op, phase): A = primary (x / g), B = w or center, C = dw.
 template <int OP, int PH, int P> struct Needs {
-  static constexpr bool loadA = (OP == OP_EASGD && PH == PH_AG);
-  static constexpr bool loadB = (OP == OP_SGD) || (OP == OP_EASGD);
-  static constexpr bool loadC = (OP == OP_SGD);
+  static constexpr bool EL = (OP == OP_EASGD) || (OP == OP_ESGD);  // elastic: a = x, b = center
+  static constexpr bool loadA = EL && PH == PH_AG;
+  static constexpr bool loadB = (OP == OP_SGD) || EL;
+  static constexpr bool loadC = (OP == OP_SGD) || (OP == OP_ESGD);
+  static constexpr bool loadD = (OP == OP_ESGD);  // the rank's own (unreduced) gradient
   // p = 1 SGD: the reduced gradient is the gradient itself -- not stored back.
   static constexpr bool storeA = !(OP == OP_SGD && PH == PH_RS && P == 1);
-  static constexpr bool storeB = (OP == OP_SGD) || (OP == OP_EASGD);
-  static constexpr bool storeC = (OP == OP_SGD);
+  static constexpr bool storeB = (OP == OP_SGD) || EL;
+  static constexpr bool storeC = (OP == OP_SGD) || (OP == OP_ESGD);
 };
 
 // SGD epilogue (A6), fp32 mirror of the oracle: t = R(R(rs*G)+R(wd*w)); dw' = R(R(mu*dw)-R(lr*t));
@@ -227,6 +229,37 @@ __device__ __forceinline__ void elem(const KParams& kp, int r, const float* in, 
       la = __fsub_rn(la, __fmul_rn(kp.alpha, dr));
       lb = in[0];  // the owner's new center
     }
+  }
+}
+
+// NEXT row f2: the elastic update (as OP_EASGD) followed in the same pass by the SGD-momentum
+// update of the elastically moved parameters with this rank's own gradient ld (one GPU per
+// client; Fig. code-snippet-4 order: Elastic2 then SGD.Update).  fp32 mirror of
+// oracle.esgd_step: xe = R(x - R(a d)), then sgd1 on (G = ld, w = xe).  Other ops: elem().
+template <int OP, int PH, int P>
+__device__ __forceinline__ void elem4(const KParams& kp, int r, const float* in, float& la,
+                                      float& lb, float& lc, float ld) {
+  if constexpr (OP == OP_ESGD) {
+    float xe;
+    if constexpr (PH == PH_RS) {
+      const float xc = lb;
+      float s = 0.f, xr = in[0];
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const float d = __fsub_rn(in[k], xc);
+        s = (k == 0) ? d : __fadd_rn(s, d);
+        if (k == r) xr = in[k];
+      }
+      xe = __fsub_rn(xr, __fmul_rn(kp.alpha, __fsub_rn(xr, xc)));
+      lb = __fadd_rn(xc, __fmul_rn(kp.alpha, s));
+    } else {
+      xe = __fsub_rn(la, __fmul_rn(kp.alpha, __fsub_rn(la, lb)));
+      lb = in[0];  // the owner's new center
+    }
+    sgd1(kp, ld, xe, lc);
+    la = xe;
+  } else {
+    elem<OP, PH, P>(kp, r, in, la, lb, lc);
   }
 }
 
@@ -1001,8 +1034,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 template <int OP>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
   using N = Needs<OP, PH_RS, 1>;
-  constexpr int NA = 1 + (N::loadB ? 1 : 0) + (N::loadC ? 1 : 0);
-  extern __shared__ __align__(128) float4 sm4[];  // [kTmaStages][3][kTileE / 4]
+  constexpr int NA = 1 + (N::loadB ? 1 : 0) + (N::loadC ? 1 : 0) + (N::loadD ? 1 : 0);
+  constexpr int NSLOT = N::loadD ? 4 : 3;  // operand slots per stage (kTmaSmem / kTmaSmem4)
+  extern __shared__ __align__(128) float4 sm4[];  // [kTmaStages][NSLOT][kTileE / 4]
   __shared__ __align__(8) uint64_t full[kTmaStages], empty[kTmaStages];
   const int r = kp.rank0 + (int)blockIdx.y;
   const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
@@ -1020,6 +1054,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
     bool ok = (n & 3) == 0 && (((uintptr_t)(kp.a[row + t] + e0)) & 15) == 0;
     if constexpr (N::loadB) ok = ok && (((uintptr_t)(kp.b[row + t] + e0)) & 15) == 0;
     if constexpr (N::loadC) ok = ok && (((uintptr_t)(kp.c[row + t] + e0)) & 15) == 0;
+    if constexpr (N::loadD) ok = ok && (((uintptr_t)(kp.d[row + t] + e0)) & 15) == 0;
     return ok;
   };
   if (warp == 0) {  // producer
@@ -1039,15 +1074,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
                        smem_u32(&full[s])),
                    "r"(NA * bytes)
                    : "memory");
-      const float* src[3] = {kp.a[row + tl.x] + tl.y,
+      const float* src[4] = {kp.a[row + tl.x] + tl.y,
                              N::loadB ? kp.b[row + tl.x] + tl.y : nullptr,
-                             N::loadC ? kp.c[row + tl.x] + tl.y : nullptr};
+                             N::loadC ? kp.c[row + tl.x] + tl.y : nullptr,
+                             N::loadD ? kp.d[row + tl.x] + tl.y : nullptr};
 #pragma unroll
-      for (int o = 0; o < 3; ++o) {
+      for (int o = 0; o < NSLOT; ++o) {
         if (src[o] == nullptr) continue;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-            "[%3];" ::"r"(smem_u32(sm4 + ((size_t)s * 3 + o) * (kTileE / 4))),
+            "[%3];" ::"r"(smem_u32(sm4 + ((size_t)s * NSLOT + o) * (kTileE / 4))),
             "l"(src[o]), "r"(bytes), "r"(smem_u32(&full[s]))
             : "memory");
       }
@@ -1062,21 +1098,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
     float* pa = kp.a[row + tl.x] + tl.y;
     float* pb = (N::loadB || N::storeB) ? kp.b[row + tl.x] + tl.y : nullptr;
     float* pc = (N::loadC || N::storeC) ? kp.c[row + tl.x] + tl.y : nullptr;
+    const float* pd = N::loadD ? kp.d[row + tl.x] + tl.y : nullptr;
     mbar_wait(&full[s], (uint32_t)((k / kTmaStages) & 1));
     if (aligned(tl.x, tl.y, tl.z)) {
-      const float4* sa = sm4 + ((size_t)s * 3 + 0) * (kTileE / 4);
-      const float4* sb = sm4 + ((size_t)s * 3 + 1) * (kTileE / 4);
-      const float4* sc = sm4 + ((size_t)s * 3 + 2) * (kTileE / 4);
+      const float4* sa = sm4 + ((size_t)s * NSLOT + 0) * (kTileE / 4);
+      const float4* sb = sm4 + ((size_t)s * NSLOT + 1) * (kTileE / 4);
+      const float4* sc = sm4 + ((size_t)s * NSLOT + 2) * (kTileE / 4);
+      const float4* sd = sm4 + ((size_t)s * NSLOT + 3) * (kTileE / 4);
       for (int v = ct; v < tl.z / 4; v += nct) {
         const float4 va = sa[v];
         float4 vb = N::loadB ? sb[v] : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 vc = N::loadC ? sc[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 vd = N::loadD ? sd[v] : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 oa;
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
           const float in[1] = {lane_of(va, l)};
           float la = 0.f, lb = lane_of(vb, l), lc = lane_of(vc, l);
-          elem<OP, PH_RS, 1>(kp, r, in, la, lb, lc);
+          elem4<OP, PH_RS, 1>(kp, r, in, la, lb, lc, lane_of(vd, l));
           lane(oa, l) = la;
           lane(vb, l) = lb;
           lane(vc, l) = lc;
@@ -1089,7 +1128,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
       for (int j = ct; j < tl.z; j += nct) {
         const float in[1] = {ld4(pa + j)};
         float la = 0.f, lb = N::loadB ? ld4(pb + j) : 0.f, lc = N::loadC ? ld4(pc + j) : 0.f;
-        elem<OP, PH_RS, 1>(kp, r, in, la, lb, lc);
+        elem4<OP, PH_RS, 1>(kp, r, in, la, lb, lc, N::loadD ? ld4(pd + j) : 0.f);
         if constexpr (N::storeA) st4(pa + j, la);
         if constexpr (N::storeB) st4(pb + j, lb);
         if constexpr (N::storeC) st4(pc + j, lc);
@@ -1118,6 +1157,7 @@ struct T2Desc {
   float* b;
   float* c;
   float* st;    // staging at the tile's first slot: my chunk (RS) or the owner's (AG)
+  const float* g;  // this rank's own gradient (ESGD), else nullptr
   int64_t e;    // element of the tile's first slot in tensor t (negative: shifted head)
   int t, n;     // tensor, slots
   int vec, pad; // 16-B aligned full slots in every operand: bulk path
@@ -1158,6 +1198,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
         d.a = kp.a[mine] + d.e;
         d.b = (N::loadB || N::storeB) ? kp.b[mine] + d.e : nullptr;
         d.c = (N::loadC || N::storeC) ? kp.c[mine] + d.e : nullptr;
+        d.g = N::loadD ? kp.d[mine] + d.e : nullptr;
         d.st = stagebuf + (size_t)(tl.y - lo) * 4;
         bool vec = d.e >= 0 && d.e + 4 * (int64_t)d.n <= kp.numel[d.t];
         int o = 0;
@@ -1170,6 +1211,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
         }
         if constexpr (N::loadB) src[o++] = d.b;
         if constexpr (N::loadC) src[o++] = d.c;
+        if constexpr (N::loadD) src[o++] = d.g;
 #pragma unroll
         for (int x = 0; x < OPSP; ++x) vec = vec && (((uintptr_t)src[x] & 15) == 0);
         vec = vec && (((uintptr_t)d.a & 15) == 0);
@@ -1233,8 +1275,8 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
           constexpr int TU = kT2Unroll;
           for (int v0 = ct; v0 < d.n; v0 += nct * TU) {
             if constexpr (PH == PH_RS) {
-              constexpr int NB = N::loadB ? 1 : 0;
-              float4 x[TU][P], b[TU], c[TU];
+              constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
+              float4 x[TU][P], b[TU], c[TU], g[TU];
 #pragma unroll
               for (int u = 0; u < TU; ++u) {
                 const int v = v0 + u * nct;
@@ -1243,6 +1285,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
                   for (int q = 0; q < P; ++q) x[u][q] = so[q * V + v];
                   b[u] = N::loadB ? so[P * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
                   c[u] = N::loadC ? so[(P + NB) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                  g[u] = N::loadD ? so[(P + NB + NC) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
               }
 #pragma unroll
@@ -1256,7 +1299,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
 #pragma unroll
                   for (int q = 0; q < P; ++q) in[q] = lane_of(x[u][q], l);
                   float la = 0.f, lb = lane_of(b[u], l), lc = lane_of(c[u], l);
-                  elem<OP, PH_RS, P>(kp, r, in, la, lb, lc);
+                  elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g[u], l));
                   lane(oa, l) = la;
                   lane(b[u], l) = lb;
                   lane(c[u], l) = lc;
@@ -1264,11 +1307,12 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
                 if constexpr (N::storeA) st16(d.a + 4 * v, oa);
                 if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
                 if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
-                st16(d.st + 4 * v, OP == OP_EASGD ? b[u] : oa);
+                st16(d.st + 4 * v, Needs<OP, PH_RS, P>::EL ? b[u] : oa);
               }
             } else {
               constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
-              float4 x[TU], a[TU], b[TU], c[TU];
+              constexpr int OD = OC + N::loadC;
+              float4 x[TU], a[TU], b[TU], c[TU], g[TU];
 #pragma unroll
               for (int u = 0; u < TU; ++u) {
                 const int v = v0 + u * nct;
@@ -1277,6 +1321,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
                   a[u] = N::loadA ? so[OA * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
                   b[u] = N::loadB ? so[OB * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
                   c[u] = N::loadC ? so[OC * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+                  g[u] = N::loadD ? so[OD * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
               }
 #pragma unroll
@@ -1287,7 +1332,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
                 for (int l = 0; l < 4; ++l) {
                   const float in[1] = {lane_of(x[u], l)};
                   float la = lane_of(a[u], l), lb = lane_of(b[u], l), lc = lane_of(c[u], l);
-                  elem<OP, PH_AG, 2>(kp, r, in, la, lb, lc);
+                  elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc, lane_of(g[u], l));
                   lane(a[u], l) = la;
                   lane(b[u], l) = lb;
                   lane(c[u], l) = lc;
@@ -1308,16 +1353,16 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
 #pragma unroll
               for (int q = 0; q < P; ++q) in[q] = ld4(kp.a[q * T + d.t] + d.e + j);
               float la = 0.f, lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
-              elem<OP, PH_RS, P>(kp, r, in, la, lb, lc);
+              elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
               if constexpr (N::storeA) st4(d.a + j, la);
               if constexpr (N::storeB) st4(d.b + j, lb);
               if constexpr (N::storeC) st4(d.c + j, lc);
-              st4(d.st + j, OP == OP_EASGD ? lb : la);
+              st4(d.st + j, Needs<OP, PH_RS, P>::EL ? lb : la);
             } else {
               const float in[1] = {ld4(d.st + j)};
               float la = N::loadA ? ld4(d.a + j) : 0.f;
               float lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
-              elem<OP, PH_AG, 2>(kp, r, in, la, lb, lc);
+              elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
               st4(d.a + j, la);
               if constexpr (N::storeB) st4(d.b + j, lb);
               if constexpr (N::storeC) st4(d.c + j, lc);
@@ -1339,8 +1384,8 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
   using NR = Needs<OP, PH_RS, P>;
   using NG = Needs<OP, PH_AG, 2>;
   constexpr int OPS = t2_ops(OP, P), NS = t2_stages(OP, P);
-  constexpr int OPS_RS = P + NR::loadB + NR::loadC;
-  constexpr int OPS_AG = 1 + NG::loadA + NG::loadB + NG::loadC;
+  constexpr int OPS_RS = P + NR::loadB + NR::loadC + NR::loadD;
+  constexpr int OPS_AG = 1 + NG::loadA + NG::loadB + NG::loadC + NG::loadD;
   constexpr int G_RS = t2_pack(OPS / OPS_RS), G_AG = t2_pack(OPS / OPS_AG);
   static_assert(OPS_RS <= OPS && OPS_AG <= OPS, "stage too small");
   extern __shared__ __align__(128) float4 sm4[];  // [NS][OPS][kT2Slots]

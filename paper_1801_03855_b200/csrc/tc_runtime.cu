@@ -328,7 +328,8 @@ tc_status grow_arena(Comm& c, int64_t need) {
 
 // ------------------------------------------------------------------ hot-path dispatcher
 tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr, float mu,
-                  float wd, float rescale, float alpha, cudaStream_t stream) {
+                  float wd, float rescale, float alpha, cudaStream_t stream,
+                  Group* gd = nullptr) {
   Comm& c = *ga->comm;
   BusyGuard busy(c.busy);
   if (!busy.ok) return TC_ERR_BUSY;
@@ -350,6 +351,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.a = ga->d_ptrs;
   kp.b = gb ? gb->d_ptrs : nullptr;
   kp.c = gc ? gc->d_ptrs : nullptr;
+  kp.d = gd ? gd->d_ptrs : nullptr;
   kp.mc = ga->d_mc;
   kp.flags = c.d_flags;
   kp.stage = c.d_stage;
@@ -375,8 +377,13 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   const int threads = c.tune_threads;
   const int64_t bytes = Mdev * 16;
   int algo;
+  // the fused elastic + SGD step (NEXT row f2) exists only in the TMA kernels
+  const int variant = op == OP_ESGD ? 0 : c.variant;
   if (p == 1) {
     algo = ALGO_LOCAL;
+  } else if (op == OP_ESGD) {
+    algo = ALGO_TWOSHOT_TMA;
+    if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   } else {
     // One-shot moves (p-1)S per GPU against 2(p-1)/p S for two-shot but needs one barrier
     // less.  Measured crossover against the TMA two-shot (config-5 sweep): p = 2 one-shot
@@ -418,7 +425,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
       return TC_ERR_CUDA;
   }
   const int nlocal = c.emulated ? p : 1;
-  int occ = max_ctas_per_sm(op, algo, p, threads, c.variant);
+  int occ = max_ctas_per_sm(op, algo, p, threads, variant);
   if (occ < 1) return TC_ERR_CUDA;
   int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
   if (cap < 1) cap = 1;
@@ -433,7 +440,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     ctas = std::max(1, std::min(ctas, std::max(tiles_r, 1)));
     kp.tiles2 = ga->d_tiles2;
     for (int q = 0; q <= p; ++q) kp.tile2_off[q] = ga->tile2_off[(size_t)q];
-  } else if (algo == ALGO_LOCAL && c.variant == 0) {  // TMA stream
+  } else if (algo == ALGO_LOCAL && variant == 0) {  // TMA stream
     ctas = std::min(ga->ntiles, c.tune_ctas > 0 ? std::min(c.tune_ctas, c.num_sms * occ)
                                                 : c.num_sms * occ);
     kp.tiles = ga->d_tiles;
@@ -454,7 +461,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (c.prof && (int64_t)ctas * nlocal <= c.prof_slots) kp.prof = c.prof;
   kp.state = c.d_state;
   cudaError_t e = launch_hot(op, algo, kp, ctas, threads, nlocal, c.emulated && p > 1, stream,
-                             c.variant);
+                             variant);
   if (e != cudaSuccess) {
     if (std::getenv("TC_DEBUG"))
       std::fprintf(stderr, "libtc: launch failed: %s\n", cudaGetErrorString(e));
@@ -462,7 +469,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   }
   c.last_algo = algo;
   c.last_ctas = ctas;
-  c.last_threads = launch_threads(op, algo, p, threads, c.variant);
+  c.last_threads = launch_threads(op, algo, p, threads, variant);
   return TC_OK;
 }
 
@@ -900,6 +907,18 @@ tc_status tc_sgd_step(tc_group* w, tc_group* g, tc_group* dw, float lr, float mo
   if (!congruent(&g->g, &w->g) || !congruent(&g->g, &dw->g)) return TC_ERR_SHAPE_MISMATCH;
   return run_hot(OP_SGD, &g->g, &w->g, &dw->g, 1.0f, lr, momentum, wd, rescale, 0,
                  (cudaStream_t)stream);
+}
+
+tc_status tc_esgd_step(tc_group* x, tc_group* center, tc_group* g, tc_group* dw, float alpha,
+                       float lr, float momentum, float wd, float rescale, void* stream) {
+  if (!x || !center || !g || !dw) return TC_ERR_INVALID_ARG;
+  if (!finite(alpha) || alpha < 0.f || alpha > 1.f || !finite(lr) || !finite(momentum) ||
+      !finite(wd) || !finite(rescale))
+    return TC_ERR_INVALID_ARG;
+  if (!congruent(&x->g, &center->g) || !congruent(&x->g, &g->g) || !congruent(&x->g, &dw->g))
+    return TC_ERR_SHAPE_MISMATCH;
+  return run_hot(OP_ESGD, &x->g, &center->g, &dw->g, 1.0f, lr, momentum, wd, rescale, alpha,
+                 (cudaStream_t)stream, &g->g);
 }
 
 tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream) {

@@ -75,6 +75,8 @@ _SIGS = {
     "tc_allreduce": (_c_int, [_vp, _c_float, _vp]),
     "tc_sgd_step": (_c_int, [_vp, _vp, _vp, _c_float, _c_float, _c_float, _c_float, _vp]),
     "tc_easgd_update": (_c_int, [_vp, _vp, _c_float, _vp]),
+    "tc_esgd_step": (_c_int, [_vp, _vp, _vp, _vp, _c_float, _c_float, _c_float, _c_float,
+                              _c_float, _vp]),
 }
 
 
@@ -383,6 +385,13 @@ def sgd_step(w: Group, g: Group, dw: Group, lr: float, momentum: float = 0.0, wd
 def easgd_update(x: Group, center: Group, alpha: float, stream=None):
     _check(LIB.tc_easgd_update(x.h, center.h, float(alpha), _stream_ptr(stream)),
            "tc_easgd_update")
+
+
+def esgd_step(x: Group, center: Group, g: Group, dw: Group, alpha: float, lr: float,
+              momentum: float = 0.0, wd: float = 0.0, rescale: float = 1.0, stream=None):
+    """NEXT row f2: elastic update then SGD-momentum with this rank's own gradient, one pass."""
+    _check(LIB.tc_esgd_step(x.h, center.h, g.h, dw.h, float(alpha), float(lr), float(momentum),
+                            float(wd), float(rescale), _stream_ptr(stream)), "tc_esgd_step")
 
 
 class BucketedStep:

@@ -70,6 +70,26 @@ def main():
             assert_bitwise(to_host(dc), wc, "easgd center")
         assert comm.async_error() == 0
 
+    # NEXT row f2: fused elastic + SGD with each rank's own gradient (one GPU per client)
+    comm.set_tuning(0, 0, -1)
+    comm.set_ll_max(-1)
+    comm.set_algorithm(0)
+    numels = [7, 13, 1000, 4096, 65, 30001]
+    center = W.group(numels, "center", 63, 0, 0, W.CENTER)
+    xs = [W.client_params(numels, center, 63, 0, i) for i in range(p)]
+    gs = [W.group(numels, "grad", 63, 1, i, W.GRAD) for i in range(p)]
+    dws = [W.group(numels, "dw", 63, 2, i, W.DW) for i in range(p)]
+    hp = dict(alpha=0.1, lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 128)
+    dx, dc, dg, dd = to_dev(xs[rank]), to_dev(center), to_dev(gs[rank]), to_dev(dws[rank])
+    with tc.Group(comm, dx) as X, tc.Group(comm, dc) as C, tc.Group(comm, dg) as G, \
+            tc.Group(comm, dd) as D:
+        tc.esgd_step(X, C, G, D, **hp)
+        wx, wc, wd = O.esgd_step(xs, center, gs, dws, **hp)
+        assert_bitwise(to_host(dx), wx[rank], "esgd x")
+        assert_bitwise(to_host(dc), wc, "esgd center")
+        assert_bitwise(to_host(dd), wd[rank], "esgd dw")
+    assert comm.async_error() == 0
+
     # symmetric (tc_mem_alloc) memory: P2P algorithms bit-exact; NVLS (switch reduction) exact on
     # integers, within the BASELINE tolerance on gradients, identical on every rank
     numels = [7, 13, 1000, 0, 50001, 3, 262144]

@@ -436,3 +436,53 @@ def test_config5_sweep_shapes(p, T):
                 assert_bitwise(to_host(views[r]), want, f"T={T} total={total} rank {r}")
             grp.destroy()
             comm.destroy()
+
+
+# ------------------------------------------------------------------ NEXT row f2: fused elastic + SGD
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_esgd_step(p, offset):
+    """tc_esgd_step (one GPU per client) bit-exact vs oracle.esgd_step: ragged groups with
+    multi-tile tensors; offset 1 shifts every tensor off its 16-B boundary (element path at
+    p = 1 heads, shifted grid at p >= 2)."""
+    numels = [7, 13, 1000, 4096, 0, 2, 3001, 9000]
+    center = W.group(numels, "center", W.CFG_EASGD, 5, 0, W.CENTER)
+    xs = [W.client_params(numels, center, W.CFG_EASGD, 5, i) for i in range(p)]
+    gs = [W.group(numels, "grad", W.CFG_EASGD, 6, i, W.GRAD) for i in range(p)]
+    dws = [W.group(numels, "dw", W.CFG_EASGD, 7, i, W.DW) for i in range(p)]
+    hp = dict(alpha=0.1, lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 128)
+    comm = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
+    dx = [to_dev(x, offset=offset) for x in xs]
+    dc = [to_dev(center, offset=offset) for _ in range(p)]
+    dg = [to_dev(g, offset=offset) for g in gs]
+    dd = [to_dev(d, offset=offset) for d in dws]
+    pick = (lambda v: v) if p > 1 else (lambda v: v[0])
+    X, C, G, D = (tc.Group(comm, pick(v)) for v in (dx, dc, dg, dd))
+    tc.esgd_step(X, C, G, D, **hp)
+    assert comm.last_launch()[0] == ("local" if p == 1 else "two-shot-tma")
+    assert comm.async_error() == 0
+    wx, wc, wd = O.esgd_step(xs, center, gs, dws, **hp)
+    for i in range(p):
+        assert_bitwise(to_host(dx[i]), wx[i], f"x client {i}")
+        assert_bitwise(to_host(dc[i]), wc, f"center replica {i}")
+        assert_bitwise(to_host(dd[i]), wd[i], f"dw client {i}")
+        assert_bitwise(to_host(dg[i]), gs[i], f"g client {i} (read only)")
+    for grp in (X, C, G, D):
+        grp.destroy()
+    comm.destroy()
+
+
+def test_esgd_step_errors():
+    comm = tc.Comm.emulated(2, 0)
+    a = [to_dev(W.group([5, 9], "grad", 1, 0, k, W.GRAD)) for k in range(2)]
+    b = [to_dev(W.group([5, 8], "grad", 1, 0, k, W.GRAD)) for k in range(2)]
+    ga, gb = tc.Group(comm, a), tc.Group(comm, b)
+    with pytest.raises(tc.TcError) as e:
+        tc.esgd_step(ga, ga, gb, ga, 0.1, 0.1)  # not congruent
+    assert e.value.status == tc.tc.TC_ERR_SHAPE_MISMATCH
+    with pytest.raises(tc.TcError) as e:
+        tc.esgd_step(ga, ga, ga, ga, 1.5, 0.1)  # alpha outside [0, 1]
+    assert e.value.status == tc.tc.TC_ERR_INVALID_ARG
+    ga.destroy()
+    gb.destroy()
+    comm.destroy()

@@ -368,3 +368,54 @@ def test_esgd_sequence_composition():
             assert Fr(float(xc[t_idx][j])) == C
             for i in range(c):
                 assert Fr(float(x[i][t_idx][j])) == X[i]
+
+
+# ------------------------------------------------------------------ NEXT row f2: esgd_step
+def test_esgd_step_exact_rational():
+    """Elastic2 then SGD.Update in one iteration, one GPU per client, c = 3, on
+    integer data with dyadic hyper-parameters: every fp32 intermediate is exact, so the oracle
+    equals the formula evaluated in exact rationals."""
+    numels = [6, 9]
+    c = 3
+    center = W.group(numels, "int", 81, 0, 0, W.CENTER)
+    xs = [W.group(numels, "int", 81, 0, i, W.PARAM) for i in range(c)]
+    gs = [W.group(numels, "int", 81, 1, i, W.GRAD) for i in range(c)]
+    dws = [W.group(numels, "int", 81, 2, i, W.DW) for i in range(c)]
+    hp = dict(alpha=0.25, lr=0.5, momentum=0.5, wd=0.25, rescale=0.125)
+    x, xc, dw = O.esgd_step(xs, center, gs, dws, **hp)
+    Fr = Fraction
+    a, lr, mu, wd, rs = (Fr(hp[k]) for k in ("alpha", "lr", "momentum", "wd", "rescale"))
+    for t, n in enumerate(numels):
+        for j in range(n):
+            C = Fr(float(center[t][j]))
+            d = [Fr(float(xs[i][t][j])) - C for i in range(c)]
+            assert Fr(float(xc[t][j])) == C + a * sum(d)
+            for i in range(c):
+                xe = Fr(float(xs[i][t][j])) - a * d[i]
+                D = mu * Fr(float(dws[i][t][j])) - lr * (rs * Fr(float(gs[i][t][j])) + wd * xe)
+                assert Fr(float(dw[i][t][j])) == D
+                assert Fr(float(x[i][t][j])) == xe + D
+
+
+def test_esgd_step_special_cases():
+    """alpha = 0: exactly the local SGD step of every client (Eq. 1 with momentum); lr = 0 and
+    momentum = 0: exactly the elastic update, with the momentum cleared."""
+    numels = [7, 13, 100]
+    c = 2
+    center = W.group(numels, "center", 82, 0, 0, W.CENTER)
+    xs = [W.client_params(numels, center, 82, 0, i) for i in range(c)]
+    gs = [W.group(numels, "grad", 82, 1, i, W.GRAD) for i in range(c)]
+    dws = [W.group(numels, "dw", 82, 2, i, W.DW) for i in range(c)]
+    x, xc, dw = O.esgd_step(xs, center, gs, dws, 0.0, 0.1, 0.9, 1e-4, 0.5)
+    for i in range(c):
+        _, w1, d1 = O.sgd_step([xs[i]], [gs[i]], [dws[i]], 0.1, 0.9, 1e-4, 0.5)
+        for t in range(len(numels)):
+            assert np.array_equal(x[i][t], w1[0][t]) and np.array_equal(dw[i][t], d1[0][t])
+    for t in range(len(numels)):
+        assert np.array_equal(xc[t], center[t])
+    x, xc, dw = O.esgd_step(xs, center, gs, dws, 0.1, 0.0, 0.0, 1e-4, 0.5)
+    xe, ce = O.easgd_update(xs, center, 0.1)
+    for t in range(len(numels)):
+        assert np.array_equal(xc[t], ce[t])
+        for i in range(c):
+            assert np.array_equal(x[i][t], xe[i][t]) and not dw[i][t].any()

@@ -15,9 +15,11 @@ whole-group tc_sgd_step, then the bucket's gradients are written.  The burst is 
 Three runs:
   compute  -- the backward pass alone;
   serial   -- backward, then one tc_sgd_step over the whole group;
-  overlap  -- tc.BucketedStep: each bucket's tc_sgd_step on a side stream once its last gradient
-              is written, with the collective kernels limited to `ctas` CTAs so the GEMMs keep
-              SMs (several budgets).
+  overlap  -- tc.BucketedStep: each bucket's collective on a side stream once its last gradient
+              is written, limited to `ctas` CTAs so the computation keeps SMs.  fused: each
+              bucket runs tc_sgd_step (allreduce + update, 6S of HBM traffic through the
+              collective's SMs); split: each bucket runs tc_allreduce (link-bound) and the
+              update runs once at the end as a full-GPU HBM stream.
 Rank 0 prints one JSON line per configuration with the fraction of the step hidden.
 """
 import argparse
@@ -182,8 +184,9 @@ def main():
     t_compute = timed(backward, a.iters, world)
     t_serial = timed(lambda: (backward(), whole_step()), a.iters, world)
     rows = []
-    for ctas in (0, 64, 32, 16):
-        step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas)
+    for split, ctas in ((False, 0), (False, 64), (True, 0), (True, 64), (True, 32), (True, 16)):
+        step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas,
+                               split=split)
         # GEMM mode: cuBLAS leaves `ctas` SMs to the collective (SM carveout), as a framework
         # overlapping communication with persistent GEMMs does
         carve = ctas if (a.compute == "gemm" and ctas) else None
@@ -198,6 +201,7 @@ def main():
         torch._C._set_sm_carveout_experimental(None)
         comm.set_tuning(0, 0, -1)
         rows.append({"bench": "overlap (NEXT row f1)", "n_gpus": world, "ctas": ctas or "auto",
+                     "mode": "split" if split else "fused",
                      "buckets": step.nbuckets, "bucket_mb": a.bucket_mb,
                      "ratio": a.ratio, "compute": a.compute, "compute_units": units,
                      "sm_carveout": carve,

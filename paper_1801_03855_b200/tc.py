@@ -395,18 +395,25 @@ def esgd_step(x: Group, center: Group, g: Group, dw: Group, alpha: float, lr: fl
 
 
 class BucketedStep:
-    """Bucketed, overlapped fused step (NEXT row f1).
+    """Bucketed, overlapped step (NEXT row f1).
 
     The gradient group is split into buckets (tc_plan_buckets, backward order).  After the
     backward pass has produced every gradient of a bucket (``grad_ready(t)`` for each of its
-    tensors, called on the compute stream in production order), the bucket's tc_sgd_step -- or
-    tc_allreduce when w/dw are None -- is enqueued on a side stream behind an event, so the
-    reduction and update of early buckets overlap the backward computation of later layers.
-    ``finish()`` makes the compute stream wait for all buckets.  All ranks must produce the
-    gradients in the same order (the bucket calls are collective).
+    tensors, called on the compute stream in production order), the bucket's collective is
+    enqueued on a side stream behind an event, so it overlaps the backward computation of later
+    layers.  ``finish()`` makes the compute stream wait for all buckets.  All ranks must produce
+    the gradients in the same order (the bucket calls are collective).
+
+    fused (split=False): each bucket runs tc_sgd_step (allreduce + update in one kernel), or
+    tc_allreduce when w/dw are None.
+    split (split=True): each bucket runs only tc_allreduce (link-bound, few SMs suffice:
+    ``ctas``), and finish() runs the SGD update once over the whole group as a local HBM
+    stream (tc_sgd_step on a single-rank comm).  Bit-identical to the fused step: the allreduce
+    rounds the float64 sum once and the local step's "sum" of one rank is that value.
     """
 
-    def __init__(self, comm, g, w=None, dw=None, bucket_bytes=25 << 20, stream=None, ctas=0):
+    def __init__(self, comm, g, w=None, dw=None, bucket_bytes=25 << 20, stream=None, ctas=0,
+                 split=False):
         import torch
         numels = [t.numel() for t in (g[0] if comm.is_emulated else g)]
         plan = Plan(numels)
@@ -421,10 +428,24 @@ class BucketedStep:
         def pick(ts, idx):
             return [[x[i] for i in idx] for x in ts] if comm.is_emulated else [ts[i] for i in idx]
 
+        self.split = bool(split) and w is not None
         self.G = [Group(comm, pick(g, m)) for m in members]
-        self.W = [Group(comm, pick(w, m)) for m in members] if w is not None else None
-        self.D = [Group(comm, pick(dw, m)) for m in members] if dw is not None else None
+        self.W = self.D = None
+        self.local = []
+        if self.split:
+            # the update after the last bucket: one local HBM stream per rank of this process
+            self.lcomm = Comm.single(g[0][0].device.index if comm.is_emulated
+                                     else g[0].device.index)
+            ranks = range(comm.nranks) if comm.is_emulated else [None]
+            for k in ranks:
+                sel = (lambda x: x[k]) if k is not None else (lambda x: x)
+                self.local.append((Group(self.lcomm, sel(w)), Group(self.lcomm, sel(g)),
+                                   Group(self.lcomm, sel(dw))))
+        elif w is not None:
+            self.W = [Group(comm, pick(w, m)) for m in members]
+            self.D = [Group(comm, pick(dw, m)) for m in members]
         self.ctas = ctas
+        self.hp = {}
         self.reset()
 
     def reset(self):
@@ -434,6 +455,7 @@ class BucketedStep:
         """Tensor t's gradient has been written (on compute_stream).  Launches its bucket's
         collective when it was the bucket's last tensor."""
         import torch
+        self.hp = hp
         b = self.bucket_of[t]
         self.missing[b] -= 1
         if self.missing[b]:
@@ -446,16 +468,20 @@ class BucketedStep:
         if self.W is not None:
             sgd_step(self.W[b], self.G[b], self.D[b], stream=self.stream, **hp)
         else:
-            allreduce(self.G[b], hp.get("scale", 1.0), stream=self.stream)
+            allreduce(self.G[b], 1.0 if self.split else hp.get("scale", 1.0), stream=self.stream)
 
     def finish(self, compute_stream=None):
         import torch
+        for W, G, D in self.local:
+            sgd_step(W, G, D, stream=self.stream, **self.hp)
         ev = torch.cuda.Event()
         ev.record(self.stream)
         (compute_stream or torch.cuda.current_stream()).wait_event(ev)
         self.reset()
 
     def destroy(self):
-        for gs in (self.G, self.W or [], self.D or []):
+        for gs in (self.G, self.W or [], self.D or [], [x for t in self.local for x in t]):
             for grp in gs:
                 grp.destroy()
+        if self.local:
+            self.lcomm.destroy()

@@ -16,8 +16,10 @@ from gpu_util import to_dev, to_host, assert_bitwise  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("p,bucket_bytes", [(3, 64 << 10), (4, 1 << 20), (2, 16)])
-def test_bucketed_sgd_matches_whole_group(p, bucket_bytes):
+def test_bucketed_sgd_matches_whole_group(p, bucket_bytes, split):
+    """fused: tc_sgd_step per bucket; split: tc_allreduce per bucket, then one local update."""
     numels = [7, 13, 1000, 4096, 65, 30000, 3, 512, 20000]
     gs = [W.group(numels, "grad", 57, 0, k, W.GRAD) for k in range(p)]
     w = W.group(numels, "param", 57, 0, 0, W.PARAM)
@@ -26,7 +28,7 @@ def test_bucketed_sgd_matches_whole_group(p, bucket_bytes):
     dg = [to_dev([np.zeros_like(a) for a in gs[k]]) for k in range(p)]
     dwt = [to_dev(w) for _ in range(p)]
     ddw = [to_dev(dw) for _ in range(p)]
-    step = tc.BucketedStep(comm, dg, dwt, ddw, bucket_bytes=bucket_bytes)
+    step = tc.BucketedStep(comm, dg, dwt, ddw, bucket_bytes=bucket_bytes, split=split)
     assert step.nbuckets >= 1
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
     compute = torch.cuda.current_stream()

@@ -207,7 +207,10 @@ TC_API int tc_comm_multicast_supported(const tc_comm* comm);
  * emulated comm `ptrs` holds nranks*ntensors pointers, rank-major (ptrs[r*ntensors + t]).
  * Nothing is copied: each pointer's cudaMalloc allocation is exported with CUDA IPC and
  * mapped by every peer (allocations shared by several tensors are mapped once).  Tensors whose
- * pointers are 16-byte aligned on every rank use 16-byte vector loads; others a scalar path.
+ * pointers sit the same number of elements past a 16-byte boundary on every rank use 16-byte
+ * vector (and TMA bulk) copies; others a scalar path.  The bulk copies may READ (never write)
+ * the rest of the 16-byte block holding a tensor's first or last element, which lies inside
+ * the same allocation for every CUDA allocator (bases 256-B aligned, sizes rounded up).
  * Errors: TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH (ranks disagree on T or any n_t; returned
  * on every rank), TC_ERR_NOT_SHAREABLE (e.g. PyTorch expandable_segments allocations),
  * TC_ERR_CUDA, TC_ERR_BOOTSTRAP. */

@@ -1200,7 +1200,12 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
         d.c = (N::loadC || N::storeC) ? kp.c[mine] + d.e : nullptr;
         d.g = N::loadD ? kp.d[mine] + d.e : nullptr;
         d.st = stagebuf + (size_t)(tl.y - lo) * 4;
-        bool vec = d.e >= 0 && d.e + 4 * (int64_t)d.n <= kp.numel[d.t];
+        // full slots, or one partial slot (a shifted tensor's head, a tail) whose containing
+        // 16-B block is bulk-copied whole (it lies inside the tensor's allocation: the
+        // allocation base is 256-B aligned and sizes are rounded to 512 B), lanes outside the
+        // tensor computed but never stored
+        const bool part = d.e < 0 || d.e + 4 * (int64_t)d.n > kp.numel[d.t];
+        bool vec = !part || d.n == 1;
         int o = 0;
         if constexpr (PH == PH_RS) {
 #pragma unroll
@@ -1215,7 +1220,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
 #pragma unroll
         for (int x = 0; x < OPSP; ++x) vec = vec && (((uintptr_t)src[x] & 15) == 0);
         vec = vec && (((uintptr_t)d.a & 15) == 0);
-        d.vec = vec;
+        d.vec = vec ? (part ? 2 : 1) : 0;
         bytes = vec ? (uint32_t)d.n * 16 * OPSP : 0;
       }
       const int bc = min(32, cnt - base);
@@ -1270,7 +1275,53 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
       }
       for (int jt = 0; jt < ut; ++jt) {
         const T2Desc d = desc[s][jt];
-        if (d.vec) {
+        if (d.vec == 2) {
+          // one partial slot from shared memory: valid lanes [lo_l, hi_l) are stored
+          if (ct == 0) {
+            const float4* so = stage(s, jt * OPSP);
+            const int lo_l = d.e < 0 ? (int)-d.e : 0;
+            const int hi_l = (int)min((int64_t)4, kp.numel[d.t] - d.e);
+            if constexpr (PH == PH_RS) {
+              constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
+              float4 b = N::loadB ? so[P * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+              float4 c = N::loadC ? so[(P + NB) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+              const float4 g = N::loadD ? so[(P + NB + NC) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+              float4 oa = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int l = 0; l < 4; ++l) {
+                if (l < lo_l || l >= hi_l) continue;
+                float in[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) in[q] = lane_of(so[q * V], l);
+                float la = 0.f, lb = lane_of(b, l), lc = lane_of(c, l);
+                elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g, l));
+                lane(oa, l) = la;
+                lane(b, l) = lb;
+                if constexpr (N::storeA) st4(d.a + l, la);
+                if constexpr (N::storeB) st4(d.b + l, lb);
+                if constexpr (N::storeC) st4(d.c + l, lc);
+              }
+              st16(d.st, Needs<OP, PH_RS, P>::EL ? b : oa);
+            } else {
+              constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
+              constexpr int OD = OC + N::loadC;
+              const float4 x = so[0];
+#pragma unroll
+              for (int l = 0; l < 4; ++l) {
+                if (l < lo_l || l >= hi_l) continue;
+                const float in[1] = {lane_of(x, l)};
+                float la = N::loadA ? lane_of(so[OA * V], l) : 0.f;
+                float lb = N::loadB ? lane_of(so[OB * V], l) : 0.f;
+                float lc = N::loadC ? lane_of(so[OC * V], l) : 0.f;
+                elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc,
+                                    N::loadD ? lane_of(so[OD * V], l) : 0.f);
+                st4(d.a + l, la);
+                if constexpr (N::storeB) st4(d.b + l, lb);
+                if constexpr (N::storeC) st4(d.c + l, lc);
+              }
+            }
+          }
+        } else if (d.vec) {
           const float4* so = stage(s, jt * OPSP);
           constexpr int TU = kT2Unroll;
           for (int v0 = ct; v0 < d.n; v0 += nct * TU) {
@@ -1422,8 +1473,14 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
   stamp(kp, 4);
   if (kp.prof != nullptr && threadIdx.x < 32)  // producer lanes each timed their own waits
     for (int o = 16; o > 0; o >>= 1) waited += __shfl_xor_sync(0xffffffffu, waited, o);
-  if (kp.prof != nullptr && (threadIdx.x == 0 || threadIdx.x == 32))
-    kp.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (threadIdx.x ? 7 : 6)] = waited;
+  if (kp.prof != nullptr && (threadIdx.x == 0 || threadIdx.x == 32)) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    // slot 6: producer waits for free stages; slot 7: consumer waits for data (low 40 bits) and
+    // the SM the CTA ran on (high bits)
+    kp.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (threadIdx.x ? 7 : 6)] =
+        threadIdx.x ? (waited & ((1ull << 40) - 1)) | ((unsigned long long)smid << 40) : waited;
+  }
   call_end(kp, r);
   stamp(kp, 5);
 }

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--algo", type=int, default=1)
     ap.add_argument("--sym", action="store_true", help="gradients in tc_mem_alloc memory")
+    ap.add_argument("--smid", action="store_true", help="TMA two-shot: RS time by SM")
     a = ap.parse_args()
     dist.init_process_group("gloo")
     rank, p = dist.get_rank(), dist.get_world_size()
@@ -66,8 +67,17 @@ def main():
         span = (t[:, 5].max() - t[:, 0].min()) / 1e3
         line = " ".join(f"{n}={np.median(d[:, i]):7.1f}/{d[:, i].max():7.1f}" for i, n in enumerate(names))
         if a.algo == 6:  # TMA two-shot: producer waiting for free stages / consumers for data
+            wf = t[:, 7] & ((1 << 40) - 1)
+            smid = t[:, 7] >> 40
             line += (f" | wait_empty={np.median(t[:, 6]) / 1e3:7.1f}"
-                     f" wait_full={np.median(t[:, 7]) / 1e3:7.1f}")
+                     f" wait_full={np.median(wf) / 1e3:7.1f}")
+            if a.smid:
+                rs = d[:, 1]
+                order = np.argsort(rs)
+                line += ("\n   RS by SM (fast..slow): " +
+                         " ".join(f"{smid[i]}:{rs[i]:.0f}" for i in order[::max(1, len(order) // 24)]) +
+                         f"\n   mean RS on SMs < 74: {rs[smid < 74].mean():.1f}, >= 74: {rs[smid >= 74].mean():.1f}"
+                         f"; even SM: {rs[smid % 2 == 0].mean():.1f}, odd: {rs[smid % 2 == 1].mean():.1f}")
         msg = (f"rank {rank} algo{a.algo} {op:9s} ctas={ctas} thr={thr} span={span:7.1f}us "
                f"(busbw@span {S * 2 * (p - 1) / p / span / 1e3:6.1f} GB/s) | med/max us: {line}")
         for r in range(p):

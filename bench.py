@@ -436,23 +436,62 @@ def main():
     # tc_sgd_step, D2H of the updated parameters.
     e2e = None
     if not args.no_e2e:
+        # Every step copies its gradients in from pinned host memory and the updated
+        # parameters out.  The copies are pipelined the way a training loop would: the next
+        # step's gradients travel H2D (into the other of two gradient buffers) while this step's
+        # kernel runs and its parameters travel D2H; a step's kernel waits for its gradients and
+        # for the previous parameter read-out (it overwrites w).
         h_g = gp_flat.cpu().pin_memory()
         h_w = torch.empty_like(w_flat, device="cpu").pin_memory()
+        if sym:
+            g2_flat = comm.alloc_symmetric(sum(numels))
+        else:
+            g2_flat = torch.empty_like(g_flat)
+        g2 = list(torch.split(g2_flat, [int(n) for n in numels]))
+        bufs, groups = [g_flat, g2_flat], [G, tc.Group(comm, g2)]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         Ke = min(K, 20)
-        with torch.cuda.stream(stream):
-            for it in range(2 + Ke):
-                if it == 2:
-                    barrier(world)
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                g_flat.copy_(h_g, non_blocking=True)
-                step()
-                h_w.copy_(w_flat, non_blocking=True)
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        for rep in range(2):  # rep 0 = warm-up
+            barrier(world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s_in.wait_stream(stream)
+            s_out.wait_stream(stream)
+            h2d_done, k_done, d2h_done = [None] * Ke, [None] * Ke, [None] * Ke
+            with torch.cuda.stream(s_in):
+                bufs[0].copy_(h_g, non_blocking=True)
+                h2d_done[0] = ev()
+                h2d_done[0].record(s_in)
+            for i in range(Ke):
+                if i + 1 < Ke:  # next step's gradients, into the buffer step i-1 used
+                    with torch.cuda.stream(s_in):
+                        if i >= 1:
+                            s_in.wait_event(k_done[i - 1])
+                        bufs[(i + 1) % 2].copy_(h_g, non_blocking=True)
+                        h2d_done[i + 1] = ev()
+                        h2d_done[i + 1].record(s_in)
+                stream.wait_event(h2d_done[i])
+                if i >= 1:
+                    stream.wait_event(d2h_done[i - 1])
+                tc.sgd_step(Wg, groups[i % 2], D, stream=stream, **hp)
+                k_done[i] = ev()
+                k_done[i].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(k_done[i])
+                    h_w.copy_(w_flat, non_blocking=True)
+                    d2h_done[i] = ev()
+                    d2h_done[i].record(s_out)
+            stream.wait_event(d2h_done[Ke - 1])
             e1.record(stream)
             stream.synchronize()
         tt = max_over_ranks(e0.elapsed_time(e1) / Ke, world) / 1e3
         e2e = {"value": p * S / tt / 1e9, "unit": UNIT, "h2d_bytes_per_step": S,
-               "d2h_bytes_per_step": S, "ms_per_step": tt * 1e3}
+               "d2h_bytes_per_step": S, "ms_per_step": tt * 1e3,
+               "pipelining": "H2D of step i+1 overlaps step i's kernel and D2H"}
+        groups[1].destroy()
+        if sym:
+            comm.free_symmetric(g2_flat)
 
     cpu = None
     if rank == 0 and p == 1 and not args.no_cpu_baseline:

@@ -24,6 +24,11 @@ Pins (tests/test_oracle_pins.py, -m "not gpu"):
                       alpha=0 identity; conservation; contraction; exact rational arithmetic.
   slot_partition   -- pinned: exact integer invariants (cover, disjoint, balance).
   esgd_sequence    -- composed of the three pinned parts (no closed form).
+  esgd_step        -- NEXT row f2 (elastic then SGD with each client's own gradient): pinned by
+                      exact rational evaluation on dyadic data and its special cases (alpha = 0
+                      -> local sgd_step; lr = momentum = 0 -> easgd_update).
+  The momentum term (mu != 0) follows reading R12; the paper fixes no formula for it, so for
+  that term alone: parity unpinned (to the paper) -- only to R12's own closed form.
 """
 from __future__ import annotations
 
@@ -31,7 +36,7 @@ import numpy as np
 
 __all__ = [
     "allreduce", "allreduce_f64", "reduce_scatter", "allgather",
-    "sgd_step", "sgd_step_f64", "easgd_update", "easgd_update_f64", "esgd_sequence",
+    "sgd_step", "sgd_step_f64", "easgd_update", "easgd_update_f64", "esgd_sequence", "esgd_step",
     "slot_partition", "bus_bytes_per_rank", "predict_cost", "ring_allreduce_sim",
     "F", "R",
 ]

@@ -1173,7 +1173,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
                                          T2Desc (*desc)[8], float4* sm4,
                                          unsigned long long& waited) {
   using N = Needs<OP, PH, PH == PH_RS ? P : 2>;
-  constexpr int V = kT2Slots;
+  constexpr int V = t2_slots(P);
   const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   const size_t T = (size_t)kp.T;
   const int lo = (int)((int64_t)kp.M * qo / P);
@@ -1439,7 +1439,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
   constexpr int OPS_AG = 1 + NG::loadA + NG::loadB + NG::loadC + NG::loadD;
   constexpr int G_RS = t2_pack(OPS / OPS_RS), G_AG = t2_pack(OPS / OPS_AG);
   static_assert(OPS_RS <= OPS && OPS_AG <= OPS, "stage too small");
-  extern __shared__ __align__(128) float4 sm4[];  // [NS][OPS][kT2Slots]
+  extern __shared__ __align__(128) float4 sm4[];  // [NS][OPS][t2_slots(P)]
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   __shared__ T2Desc desc[NS][8];
   const int r = kp.rank0 + (int)blockIdx.y;

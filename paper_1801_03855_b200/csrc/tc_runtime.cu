@@ -251,8 +251,8 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
         const int64_t full_end = end - (((n + m) & 3) ? 1 : 0);
         if (a < first_full) tiles.push_back(make_int4(u, (int)a++, 1, 0));
         const int64_t vend = std::min(b, full_end);
-        for (int64_t x = a; x < vend; x += kT2Slots)
-          tiles.push_back(make_int4(u, (int)x, (int)std::min<int64_t>(kT2Slots, vend - x), 0));
+        for (int64_t x = a; x < vend; x += t2_slots(p))
+          tiles.push_back(make_int4(u, (int)x, (int)std::min<int64_t>(t2_slots(p), vend - x), 0));
         const int64_t rest = std::max(a, vend);
         if (b > rest) tiles.push_back(make_int4(u, (int)rest, (int)(b - rest), 0));
       }

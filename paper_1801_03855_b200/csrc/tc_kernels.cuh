@@ -1167,6 +1167,159 @@ __host__ __device__ constexpr int t2_pack(int x) {
   return x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1;
 }
 
+// One tile of a TMA two-shot phase, processed by the consumer warps: a full tile and a partial
+// slot from shared memory (operand o of this tile at so + o * V), the element path from global
+// memory.
+template <int OP, int P, int PH, int OPSP, int V>
+__device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& d,
+                                        const float4* so, int ct, int nct) {
+  using N = Needs<OP, PH, PH == PH_RS ? P : 2>;
+  const size_t T = (size_t)kp.T;
+  if (d.vec == 2) {
+    // one partial slot from shared memory: valid lanes [lo_l, hi_l) are stored
+    if (ct == 0) {
+      const int lo_l = d.e < 0 ? (int)-d.e : 0;
+      const int hi_l = (int)min((int64_t)4, kp.numel[d.t] - d.e);
+      if constexpr (PH == PH_RS) {
+        constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
+        float4 b = N::loadB ? so[P * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 c = N::loadC ? so[(P + NB) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 g = N::loadD ? so[(P + NB + NC) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 oa = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          if (l < lo_l || l >= hi_l) continue;
+          float in[P];
+#pragma unroll
+          for (int q = 0; q < P; ++q) in[q] = lane_of(so[q * V], l);
+          float la = 0.f, lb = lane_of(b, l), lc = lane_of(c, l);
+          elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g, l));
+          lane(oa, l) = la;
+          lane(b, l) = lb;
+          if constexpr (N::storeA) st4(d.a + l, la);
+          if constexpr (N::storeB) st4(d.b + l, lb);
+          if constexpr (N::storeC) st4(d.c + l, lc);
+        }
+        st16(d.st, Needs<OP, PH_RS, P>::EL ? b : oa);
+      } else {
+        constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
+        constexpr int OD = OC + N::loadC;
+        const float4 x = so[0];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          if (l < lo_l || l >= hi_l) continue;
+          const float in[1] = {lane_of(x, l)};
+          float la = N::loadA ? lane_of(so[OA * V], l) : 0.f;
+          float lb = N::loadB ? lane_of(so[OB * V], l) : 0.f;
+          float lc = N::loadC ? lane_of(so[OC * V], l) : 0.f;
+          elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc,
+                              N::loadD ? lane_of(so[OD * V], l) : 0.f);
+          st4(d.a + l, la);
+          if constexpr (N::storeB) st4(d.b + l, lb);
+          if constexpr (N::storeC) st4(d.c + l, lc);
+        }
+      }
+    }
+  } else if (d.vec) {
+        constexpr int TU = kT2Unroll;
+    for (int v0 = ct; v0 < d.n; v0 += nct * TU) {
+      if constexpr (PH == PH_RS) {
+        constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
+        float4 x[TU][P], b[TU], c[TU], g[TU];
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          const int v = v0 + u * nct;
+          if (v < d.n) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) x[u][q] = so[q * V + v];
+            b[u] = N::loadB ? so[P * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            c[u] = N::loadC ? so[(P + NB) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            g[u] = N::loadD ? so[(P + NB + NC) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          const int v = v0 + u * nct;
+          if (v >= d.n) continue;
+          float4 oa;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            float in[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) in[q] = lane_of(x[u][q], l);
+            float la = 0.f, lb = lane_of(b[u], l), lc = lane_of(c[u], l);
+            elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g[u], l));
+            lane(oa, l) = la;
+            lane(b[u], l) = lb;
+            lane(c[u], l) = lc;
+          }
+          if constexpr (N::storeA) st16(d.a + 4 * v, oa);
+          if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
+          if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
+          st16(d.st + 4 * v, Needs<OP, PH_RS, P>::EL ? b[u] : oa);
+        }
+      } else {
+        constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
+        constexpr int OD = OC + N::loadC;
+        float4 x[TU], a[TU], b[TU], c[TU], g[TU];
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          const int v = v0 + u * nct;
+          if (v < d.n) {
+            x[u] = so[v];
+            a[u] = N::loadA ? so[OA * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            b[u] = N::loadB ? so[OB * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            c[u] = N::loadC ? so[OC * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            g[u] = N::loadD ? so[OD * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          const int v = v0 + u * nct;
+          if (v >= d.n) continue;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const float in[1] = {lane_of(x[u], l)};
+            float la = lane_of(a[u], l), lb = lane_of(b[u], l), lc = lane_of(c[u], l);
+            elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc, lane_of(g[u], l));
+            lane(a[u], l) = la;
+            lane(b[u], l) = lb;
+            lane(c[u], l) = lc;
+          }
+          st16(d.a + 4 * v, a[u]);
+          if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
+          if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
+        }
+      }
+    }
+  } else {
+    // element path (shifted heads, partial tails, operands misaligned on some rank)
+    const int64_t j0 = d.e < 0 ? -d.e : 0;
+    const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
+    for (int64_t j = j0 + ct; j < j1; j += nct) {
+      if constexpr (PH == PH_RS) {
+        float in[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) in[q] = ld4(kp.a[q * T + d.t] + d.e + j);
+        float la = 0.f, lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
+        elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
+        if constexpr (N::storeA) st4(d.a + j, la);
+        if constexpr (N::storeB) st4(d.b + j, lb);
+        if constexpr (N::storeC) st4(d.c + j, lc);
+        st4(d.st + j, Needs<OP, PH_RS, P>::EL ? lb : la);
+      } else {
+        const float in[1] = {ld4(d.st + j)};
+        float la = N::loadA ? ld4(d.a + j) : 0.f;
+        float lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
+        elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
+        st4(d.a + j, la);
+        if constexpr (N::storeB) st4(d.b + j, lb);
+        if constexpr (N::storeC) st4(d.c + j, lc);
+      }
+    }
+  }
+}
+
 template <int OP, int P, int PH, int G, int OPSP, int OPS, int NS>
 __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float* stagebuf,
                                          int& k, uint64_t* full, uint64_t* empty,
@@ -1273,154 +1426,8 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
         mbar_wait(&full[s], (uint32_t)((k / NS) & 1));
         if (kp.prof) waited += globaltimer() - t0;
       }
-      for (int jt = 0; jt < ut; ++jt) {
-        const T2Desc d = desc[s][jt];
-        if (d.vec == 2) {
-          // one partial slot from shared memory: valid lanes [lo_l, hi_l) are stored
-          if (ct == 0) {
-            const float4* so = stage(s, jt * OPSP);
-            const int lo_l = d.e < 0 ? (int)-d.e : 0;
-            const int hi_l = (int)min((int64_t)4, kp.numel[d.t] - d.e);
-            if constexpr (PH == PH_RS) {
-              constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
-              float4 b = N::loadB ? so[P * V] : make_float4(0.f, 0.f, 0.f, 0.f);
-              float4 c = N::loadC ? so[(P + NB) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
-              const float4 g = N::loadD ? so[(P + NB + NC) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
-              float4 oa = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-              for (int l = 0; l < 4; ++l) {
-                if (l < lo_l || l >= hi_l) continue;
-                float in[P];
-#pragma unroll
-                for (int q = 0; q < P; ++q) in[q] = lane_of(so[q * V], l);
-                float la = 0.f, lb = lane_of(b, l), lc = lane_of(c, l);
-                elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g, l));
-                lane(oa, l) = la;
-                lane(b, l) = lb;
-                if constexpr (N::storeA) st4(d.a + l, la);
-                if constexpr (N::storeB) st4(d.b + l, lb);
-                if constexpr (N::storeC) st4(d.c + l, lc);
-              }
-              st16(d.st, Needs<OP, PH_RS, P>::EL ? b : oa);
-            } else {
-              constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
-              constexpr int OD = OC + N::loadC;
-              const float4 x = so[0];
-#pragma unroll
-              for (int l = 0; l < 4; ++l) {
-                if (l < lo_l || l >= hi_l) continue;
-                const float in[1] = {lane_of(x, l)};
-                float la = N::loadA ? lane_of(so[OA * V], l) : 0.f;
-                float lb = N::loadB ? lane_of(so[OB * V], l) : 0.f;
-                float lc = N::loadC ? lane_of(so[OC * V], l) : 0.f;
-                elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc,
-                                    N::loadD ? lane_of(so[OD * V], l) : 0.f);
-                st4(d.a + l, la);
-                if constexpr (N::storeB) st4(d.b + l, lb);
-                if constexpr (N::storeC) st4(d.c + l, lc);
-              }
-            }
-          }
-        } else if (d.vec) {
-          const float4* so = stage(s, jt * OPSP);
-          constexpr int TU = kT2Unroll;
-          for (int v0 = ct; v0 < d.n; v0 += nct * TU) {
-            if constexpr (PH == PH_RS) {
-              constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
-              float4 x[TU][P], b[TU], c[TU], g[TU];
-#pragma unroll
-              for (int u = 0; u < TU; ++u) {
-                const int v = v0 + u * nct;
-                if (v < d.n) {
-#pragma unroll
-                  for (int q = 0; q < P; ++q) x[u][q] = so[q * V + v];
-                  b[u] = N::loadB ? so[P * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-                  c[u] = N::loadC ? so[(P + NB) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-                  g[u] = N::loadD ? so[(P + NB + NC) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < TU; ++u) {
-                const int v = v0 + u * nct;
-                if (v >= d.n) continue;
-                float4 oa;
-#pragma unroll
-                for (int l = 0; l < 4; ++l) {
-                  float in[P];
-#pragma unroll
-                  for (int q = 0; q < P; ++q) in[q] = lane_of(x[u][q], l);
-                  float la = 0.f, lb = lane_of(b[u], l), lc = lane_of(c[u], l);
-                  elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g[u], l));
-                  lane(oa, l) = la;
-                  lane(b[u], l) = lb;
-                  lane(c[u], l) = lc;
-                }
-                if constexpr (N::storeA) st16(d.a + 4 * v, oa);
-                if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
-                if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
-                st16(d.st + 4 * v, Needs<OP, PH_RS, P>::EL ? b[u] : oa);
-              }
-            } else {
-              constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
-              constexpr int OD = OC + N::loadC;
-              float4 x[TU], a[TU], b[TU], c[TU], g[TU];
-#pragma unroll
-              for (int u = 0; u < TU; ++u) {
-                const int v = v0 + u * nct;
-                if (v < d.n) {
-                  x[u] = so[v];
-                  a[u] = N::loadA ? so[OA * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-                  b[u] = N::loadB ? so[OB * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-                  c[u] = N::loadC ? so[OC * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-                  g[u] = N::loadD ? so[OD * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < TU; ++u) {
-                const int v = v0 + u * nct;
-                if (v >= d.n) continue;
-#pragma unroll
-                for (int l = 0; l < 4; ++l) {
-                  const float in[1] = {lane_of(x[u], l)};
-                  float la = lane_of(a[u], l), lb = lane_of(b[u], l), lc = lane_of(c[u], l);
-                  elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc, lane_of(g[u], l));
-                  lane(a[u], l) = la;
-                  lane(b[u], l) = lb;
-                  lane(c[u], l) = lc;
-                }
-                st16(d.a + 4 * v, a[u]);
-                if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
-                if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
-              }
-            }
-          }
-        } else {
-          // element path (shifted heads, partial tails, operands misaligned on some rank)
-          const int64_t j0 = d.e < 0 ? -d.e : 0;
-          const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
-          for (int64_t j = j0 + ct; j < j1; j += nct) {
-            if constexpr (PH == PH_RS) {
-              float in[P];
-#pragma unroll
-              for (int q = 0; q < P; ++q) in[q] = ld4(kp.a[q * T + d.t] + d.e + j);
-              float la = 0.f, lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
-              elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
-              if constexpr (N::storeA) st4(d.a + j, la);
-              if constexpr (N::storeB) st4(d.b + j, lb);
-              if constexpr (N::storeC) st4(d.c + j, lc);
-              st4(d.st + j, Needs<OP, PH_RS, P>::EL ? lb : la);
-            } else {
-              const float in[1] = {ld4(d.st + j)};
-              float la = N::loadA ? ld4(d.a + j) : 0.f;
-              float lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
-              elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
-              st4(d.a + j, la);
-              if constexpr (N::storeB) st4(d.b + j, lb);
-              if constexpr (N::storeC) st4(d.c + j, lc);
-            }
-          }
-        }
-      }
+      for (int jt = 0; jt < ut; ++jt)
+        t2_tile<OP, P, PH, OPSP, V>(kp, r, desc[s][jt], stage(s, jt * OPSP), ct, nct);
       __syncwarp();
       if (lane_id == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))

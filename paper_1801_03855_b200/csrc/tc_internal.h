@@ -82,7 +82,8 @@ enum Algo {
   ALGO_TWOSHOT_PUSH = 3,
   ALGO_NVLS = 4,
   ALGO_LL = 5,
-  ALGO_TWOSHOT_TMA = 6
+  ALGO_TWOSHOT_TMA = 6,
+  ALGO_TWOSHOT_BAL = 7
 };
 
 // ---------------------------------------------------------------- A1 descriptor (host)
@@ -115,6 +116,9 @@ tc_status bootstrap_allgather(tc_allgather_fn ag, void* ctx, int nranks, const v
 struct DevState {
   uint32_t epoch;
   uint32_t done;
+  uint32_t ctr_rs, ctr_ag;  // balanced TMA two-shot: next unclaimed tile of each phase
+  uint32_t done_rs;         // CTAs that finished the reduce-scatter
+  uint32_t pad;
 };
 
 // Passed by value to every hot-path kernel.  Tables are device arrays.

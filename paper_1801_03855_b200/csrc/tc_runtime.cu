@@ -382,7 +382,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (p == 1) {
     algo = ALGO_LOCAL;
   } else if (op == OP_ESGD) {
-    algo = ALGO_TWOSHOT_TMA;
+    algo = c.algo_override == ALGO_TWOSHOT_BAL ? ALGO_TWOSHOT_BAL : ALGO_TWOSHOT_TMA;
     if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   } else {
     // One-shot moves (p-1)S per GPU against 2(p-1)/p S for two-shot but needs one barrier
@@ -412,6 +412,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;
     else if (c.algo_override == ALGO_TWOSHOT_PUSH) algo = ALGO_TWOSHOT_PUSH;
     else if (c.algo_override == ALGO_TWOSHOT_TMA) algo = ALGO_TWOSHOT_TMA;
+    else if (c.algo_override == ALGO_TWOSHOT_BAL) algo = ALGO_TWOSHOT_BAL;
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
     // (automatic NVLS only for the plain allreduce: the fused SGD step's HBM epilogue cannot
     // start before the switch has reduced a chunk, measured 405 us vs 297 us pulled at p = 4)
@@ -420,7 +421,8 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     // TMA-staged two-shot: ResNet-50 group p = 2 allreduce 188 / SGD step 197 us (LDG pull
     // 208 / 226, NCCL allreduce 219); p = 4 262 / 278 us (pull 289 / 301, NCCL 274-276).
     else algo = ALGO_TWOSHOT_TMA;
-    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH || algo == ALGO_TWOSHOT_TMA) &&
+    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH || algo == ALGO_TWOSHOT_TMA ||
+         algo == ALGO_TWOSHOT_BAL) &&
         (Mdev + p - 1) / p + 1 > c.arena_cap)
       return TC_ERR_CUDA;
   }
@@ -433,7 +435,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   int64_t work_slots = twoshot ? (Mdev + p - 1) / p : Mdev;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
-  if (algo == ALGO_TWOSHOT_TMA) {
+  if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL) {
     // bytes in flight come from the stage ring, not from threads: one CTA per SM at most
     const int tiles_r = ga->tile2_off[1] - ga->tile2_off[0];
     ctas = c.tune_ctas > 0 ? c.tune_ctas : c.num_sms;
@@ -604,7 +606,7 @@ tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes) {
 
 tc_status tc_comm_set_algorithm(tc_comm* comm, int algo) {
   if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH &&
-                algo != ALGO_NVLS && algo != ALGO_TWOSHOT_TMA))
+                algo != ALGO_NVLS && algo != ALGO_TWOSHOT_TMA && algo != ALGO_TWOSHOT_BAL))
     return TC_ERR_INVALID_ARG;
   comm->c.algo_override = algo;
   return TC_OK;

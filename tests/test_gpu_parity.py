@@ -28,8 +28,9 @@ TWOSHOT = 0         # force two-shot (pull reduce-scatter)
 PUSH = -2           # force two-shot with pushed reduce-scatter
 LL = -3             # force the low-latency algorithm
 TMA = -4            # force the TMA-staged two-shot
+BAL = -5            # force the TMA two-shot with claimed (balanced) tiles
 ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT), ("ll", LL),
-         ("two-shot-tma", TMA)]
+         ("two-shot-tma", TMA), ("two-shot-bal", BAL)]
 
 
 def _comm(p, oneshot=-1, ctas=0):
@@ -44,6 +45,9 @@ def _comm(p, oneshot=-1, ctas=0):
         oneshot = 0
     elif oneshot == TMA:
         c.set_algorithm(6)
+        oneshot = 0
+    elif oneshot == BAL:
+        c.set_algorithm(7)
         oneshot = 0
     elif oneshot == TWOSHOT and p > 1:
         c.set_algorithm(1)
@@ -107,7 +111,7 @@ def test_unaligned_tensors(p, offset):
     numels = [7, 13, 1000, 4096, 3, 1, 2]
     xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
     off = (lambda k: k % 4) if offset == "per-rank" else offset
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL):
         out, _ = run_allreduce(xs, oneshot=oneshot, offset=off)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -146,7 +150,7 @@ def test_fewer_slots_than_ranks(p):
     """N < p: some owners have empty chunks."""
     numels = [1, 2] if p == 4 else [3, 0, 1]
     xs = [W.group(numels, "int", 75, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, TMA):
+    for oneshot in (TWOSHOT, PUSH, TMA, BAL):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -157,7 +161,7 @@ def test_many_tensors_1024():
     g = np.random.default_rng(5)
     numels = W.random_numels(g, 1024, 700)
     xs = [W.group(numels, "grad", 74, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -169,7 +173,7 @@ def test_cta_counts(ctas):
     p = 3
     numels = [7, 13, 1000, 50000, 9]
     xs = [W.group(numels, "grad", 73, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, TMA):
+    for oneshot in (TWOSHOT, PUSH, TMA, BAL):
         out, _ = run_allreduce(xs, oneshot=oneshot, ctas=ctas)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -203,8 +207,8 @@ def test_repeated_calls_epochs():
     dev = [to_dev(x) for x in xs]
     grp = tc.Group(comm, dev)
     want = O.allreduce(xs, 1.0 / p)
-    for i in range(40):
-        comm.set_algorithm(3 if i % 2 else 1)
+    for i in range(60):
+        comm.set_algorithm((1, 3, 6, 7)[i % 4])
         comm.set_tuning(0, 0, ONESHOT if i % 3 == 0 else TWOSHOT)
         comm.set_ll_max(1 << 30 if i % 5 == 0 else 0)
         tc.allreduce(grp, 1.0 / p if i == 0 else 1.0 / p)
@@ -214,7 +218,7 @@ def test_repeated_calls_epochs():
     for r in range(p):
         assert_bitwise(first[r], want, "first call")
         # afterwards every rank holds the mean; averaging identical values is the identity
-        assert_bitwise(out[r], want, "after 40 calls")
+        assert_bitwise(out[r], want, "after 60 calls")
     assert comm.async_error() == 0
     grp.destroy()
     comm.destroy()
@@ -402,7 +406,7 @@ def _sampled_check(numels, outs, xs, scale, p, seed=0, per_tensor=48):
 
 @pytest.mark.parametrize("group,p,oneshot", [("resnet50", 1, -1), ("resnet50", 2, TWOSHOT),
                                              ("resnet50", 4, PUSH), ("alexnet", 2, TWOSHOT),
-                                             ("resnet50", 4, TMA)])
+                                             ("resnet50", 4, TMA), ("resnet50", 4, BAL)])
 def test_full_size_groups_sampled(group, p, oneshot):
     """Configs 2/3 at their full size (ResNet-50 25.6M, AlexNet 61.1M fp32 per rank), in the
     launch configuration bench.py times, checked on sampled outputs."""
@@ -423,7 +427,7 @@ def test_config5_sweep_shapes(p, T):
         if not numels:
             continue
         xs = [W.group(numels, "grad", W.CFG_SWEEP, 0, k, W.GRAD) for k in range(p)]
-        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL, TMA)):
+        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL, TMA, BAL)):
             if oneshot == LL and total > (64 << 10):
                 continue
             comm = _comm(p, oneshot)
@@ -441,7 +445,8 @@ def test_config5_sweep_shapes(p, T):
 # ------------------------------------------------------------------ NEXT row f2: fused elastic + SGD
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("offset", [0, 1])
-def test_esgd_step(p, offset):
+@pytest.mark.parametrize("bal", [False, True])
+def test_esgd_step(p, offset, bal):
     """tc_esgd_step (one GPU per client) bit-exact vs oracle.esgd_step: ragged groups with
     multi-tile tensors; offset 1 shifts every tensor off its 16-B boundary (element path at
     p = 1 heads, shifted grid at p >= 2)."""
@@ -452,6 +457,8 @@ def test_esgd_step(p, offset):
     dws = [W.group(numels, "dw", W.CFG_EASGD, 7, i, W.DW) for i in range(p)]
     hp = dict(alpha=0.1, lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 128)
     comm = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
+    if bal:
+        comm.set_algorithm(7)
     dx = [to_dev(x, offset=offset) for x in xs]
     dc = [to_dev(center, offset=offset) for _ in range(p)]
     dg = [to_dev(g, offset=offset) for g in gs]
@@ -459,7 +466,8 @@ def test_esgd_step(p, offset):
     pick = (lambda v: v) if p > 1 else (lambda v: v[0])
     X, C, G, D = (tc.Group(comm, pick(v)) for v in (dx, dc, dg, dd))
     tc.esgd_step(X, C, G, D, **hp)
-    assert comm.last_launch()[0] == ("local" if p == 1 else "two-shot-tma")
+    assert comm.last_launch()[0] == ("local" if p == 1 else
+                                     "two-shot-bal" if bal else "two-shot-tma")
     assert comm.async_error() == 0
     wx, wc, wd = O.esgd_step(xs, center, gs, dws, **hp)
     for i in range(p):

@@ -1,0 +1,10 @@
+export TC_TIMEOUT_MS=20000
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for NP in 2 4; do
+for A in 6 7; do
+CV=$([ $NP = 2 ] && echo 0,1 || echo 0,1,2,3)
+for c in 64 148; do
+  CUDA_VISIBLE_DEVICES=$CV timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NP --master-addr 127.0.0.1 --master-port 2971$NP tools/phase_probe.py --sym --algo $A --ctas $c 2>&1 | grep -E "rank 0" | head -2 | sed 's/(busbw.*RS=/RS=/' | sed "s/^/p=$NP /" | cut -c1-150
+done
+done
+done

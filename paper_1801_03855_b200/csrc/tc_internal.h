@@ -28,9 +28,18 @@ constexpr int kPieceShift = 7;                 // work piece = 128 slots = 2 KiB
 constexpr int kPiece = 1 << kPieceShift;
 // p = 1 TMA stream (k_local_tma): tiles of up to kTileE elements inside one tensor, kTmaStages
 // shared-memory stages of (up to) three operands, one producer warp + kTmaConsumerWarps.
-constexpr int kTileE = 2048;
-constexpr int kTmaStages = 4;
-constexpr int kTmaConsumerWarps = 8;
+#ifndef TC_TILE_E
+#define TC_TILE_E 2048
+#endif
+#ifndef TC_TMA_STAGES
+#define TC_TMA_STAGES 4
+#endif
+#ifndef TC_TMA_CW
+#define TC_TMA_CW 8
+#endif
+constexpr int kTileE = TC_TILE_E;
+constexpr int kTmaStages = TC_TMA_STAGES;
+constexpr int kTmaConsumerWarps = TC_TMA_CW;
 constexpr int kTmaThreads = 32 * (1 + kTmaConsumerWarps);
 constexpr int kTmaSmem = kTmaStages * 3 * kTileE * 4;      // three operands (SGD: g, w, dw)
 constexpr int kTmaSmem4 = kTmaStages * 4 * kTileE * 4;     // four (ESGD: x, center, dw, g)

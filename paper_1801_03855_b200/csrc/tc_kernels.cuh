@@ -864,6 +864,9 @@ __global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
   stamp(kp, 1);
   ReduceBody<OP, P, SRC_ONESHOT, false> body{kp, r, 0, nullptr};
   slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
+  stamp(kp, 2);
+  stamp(kp, 3);
+  stamp(kp, 4);
   call_end(kp, r);
   stamp(kp, 5);
 }

@@ -22,10 +22,12 @@ import tc_workloads as W  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="resnet50")
+    ap.add_argument("--numel", type=int, default=0, help="one flat tensor of this many elements")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--algo", type=int, default=1)
+    ap.add_argument("--oneshot", type=int, default=0, help="one-shot limit in bytes (-1 auto)")
     ap.add_argument("--sym", action="store_true", help="gradients in tc_mem_alloc memory")
     ap.add_argument("--smid", action="store_true", help="TMA two-shot: RS time by SM")
     a = ap.parse_args()
@@ -33,7 +35,7 @@ def main():
     rank, p = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    numels = W.GROUPS[a.config]
+    numels = W.GROUPS[a.config] if a.numel <= 0 else [a.numel]
     S = 4 * sum(numels)
 
     def flat(kind, role):
@@ -46,7 +48,7 @@ def main():
         sym = comm.alloc_symmetric(sum(numels))
         sym.copy_(torch.cat(g))
         g = list(torch.split(sym, numels))
-    comm.set_tuning(a.ctas, a.threads, 0)
+    comm.set_tuning(a.ctas, a.threads, a.oneshot)
     comm.set_algorithm(a.algo)
     prof = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
     G, Wg, D = tc.Group(comm, g), tc.Group(comm, w), tc.Group(comm, dw)

@@ -70,6 +70,18 @@ def main():
             assert_bitwise(to_host(dc), wc, "easgd center")
         assert comm.async_error() == 0
 
+    # a pointer CUDA IPC cannot export (pinned host memory on rank 0): every rank gets
+    # TC_ERR_NOT_SHAREABLE from the collective tc_group_create
+    import ctypes
+    host = torch.zeros(1024, dtype=torch.float32).pin_memory()
+    devt = torch.zeros(1024, dtype=torch.float32, device="cuda")
+    ptr = host.data_ptr() if rank == 0 else devt.data_ptr()
+    out = ctypes.c_void_p()
+    st = tc.LIB.tc_group_create(comm.h, 1, (ctypes.c_void_p * 1)(ptr),
+                                (ctypes.c_int64 * 1)(1024), ctypes.byref(out))
+    assert st == tc.tc.TC_ERR_NOT_SHAREABLE, st
+    assert not out.value
+
     # NEXT row f2: fused elastic + SGD with each rank's own gradient (one GPU per client)
     comm.set_tuning(0, 0, -1)
     comm.set_ll_max(-1)

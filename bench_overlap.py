@@ -109,7 +109,9 @@ class Burn:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ratio", type=float, default=1.0)
-    ap.add_argument("--compute", default="burn", choices=["burn", "gemm"])
+    ap.add_argument("--compute", default="gemm", choices=["burn", "gemm"])
+    ap.add_argument("--carveout", action="store_true",
+                    help="GEMM mode: leave the collective's CTAs free via cuBLASLt's SM carveout")
     ap.add_argument("--bucket-mb", type=float, default=25.0)
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
@@ -184,12 +186,12 @@ def main():
     t_compute = timed(backward, a.iters, world)
     t_serial = timed(lambda: (backward(), whole_step()), a.iters, world)
     rows = []
-    for split, ctas in ((False, 0), (False, 64), (True, 0), (True, 64), (True, 32), (True, 16)):
+    for split, ctas in ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)):
         step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas,
                                split=split)
         # GEMM mode: cuBLAS leaves `ctas` SMs to the collective (SM carveout), as a framework
         # overlapping communication with persistent GEMMs does
-        carve = ctas if (a.compute == "gemm" and ctas) else None
+        carve = ctas if (a.compute == "gemm" and ctas and a.carveout) else None
         torch._C._set_sm_carveout_experimental(carve)
 
         def overlapped():

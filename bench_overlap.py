@@ -112,7 +112,7 @@ def main():
     ap.add_argument("--compute", default="gemm", choices=["burn", "gemm"])
     ap.add_argument("--carveout", action="store_true",
                     help="GEMM mode: leave the collective's CTAs free via cuBLASLt's SM carveout")
-    ap.add_argument("--bucket-mb", type=float, default=25.0)
+    ap.add_argument("--bucket-mb", type=float, default=64.0)
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))

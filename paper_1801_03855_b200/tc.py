@@ -412,7 +412,9 @@ class BucketedStep:
     rounds the float64 sum once and the local step's "sum" of one rank is that value.
     """
 
-    def __init__(self, comm, g, w=None, dw=None, bucket_bytes=25 << 20, stream=None, ctas=0,
+    # defaults from bench_overlap.py on B200 (DESIGN.md §10): two large buckets and a 64-CTA
+    # collective hid 13% of the step at p = 4; 25 MiB buckets and the full grid hid none
+    def __init__(self, comm, g, w=None, dw=None, bucket_bytes=64 << 20, stream=None, ctas=64,
                  split=False):
         import torch
         numels = [t.numel() for t in (g[0] if comm.is_emulated else g)]

@@ -467,10 +467,15 @@ class BucketedStep:
         self.stream.wait_event(ev)
         if self.ctas:
             self.comm.set_tuning(self.ctas, 0, -1)
-        if self.W is not None:
-            sgd_step(self.W[b], self.G[b], self.D[b], stream=self.stream, **hp)
-        else:
-            allreduce(self.G[b], 1.0 if self.split else hp.get("scale", 1.0), stream=self.stream)
+        try:
+            if self.W is not None:
+                sgd_step(self.W[b], self.G[b], self.D[b], stream=self.stream, **hp)
+            else:
+                allreduce(self.G[b], 1.0 if self.split else hp.get("scale", 1.0),
+                          stream=self.stream)
+        finally:
+            if self.ctas:  # the CTA budget applies to the bucket launches only
+                self.comm.set_tuning(0, 0, -1)
 
     def finish(self, compute_stream=None):
         import torch

@@ -204,6 +204,49 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ the product arm
+def config4_sequence(args, p, rank, local, numels, dev, ecomm, cen, stream, timed_calls):
+    """BASELINE config 4 (MPI Elastic SGD, Fig. code-snippet-4): 2 clients of p/2 GPUs each;
+    every step each client runs the fused allreduce + SGD over its GPUs, and every tau = 4 steps
+    the counterpart pairs (k, k + p/2) first run the elastic update of the client parameters
+    (P:309-313).  Reports the mean step over 16 steps (4 elastic updates)."""
+    import torch.distributed as dist
+    import paper_1801_03855_b200 as tc
+    half = p // 2
+    mine = None
+    for c in range(2):
+        grp = dist.new_group(list(range(c * half, (c + 1) * half)), backend="gloo")
+        if rank // half == c:
+            mine = grp
+    ccomm = tc.Comm.single(local) if half == 1 else tc.Comm.from_process_group(mine, device=local)
+    _, w4 = dev(W.group(numels, "param", W.CFG_EASGD, 3, rank // half, W.PARAM))
+    _, g4 = dev(W.group(numels, "grad", W.CFG_EASGD, 4, rank, W.GRAD))
+    _, d4 = dev(W.group(numels, "dw", W.CFG_EASGD, 5, rank // half, W.DW))
+    W4, G4, D4 = tc.Group(ccomm, w4), tc.Group(ccomm, g4), tc.Group(ccomm, d4)
+    X4 = tc.Group(ecomm, w4)
+    C4 = tc.Group(ecomm, cen)
+    hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (half * 128))
+    steps, tau = 16, 4
+
+    def sequence():
+        for t in range(steps):
+            if t % tau == 0:
+                tc.easgd_update(X4, C4, 0.1, stream=stream)
+            tc.sgd_step(W4, G4, D4, stream=stream, **hp)
+
+    t_seq = timed_calls(sequence)
+    t_sgd = timed_calls(lambda: tc.sgd_step(W4, G4, D4, stream=stream, **hp))
+    out = {"clients": 2, "gpus_per_client": half, "tau": tau, "steps": steps,
+           "mean_step_us": t_seq / steps, "sgd_step_us": t_sgd,
+           "easgd_amortised_us": t_seq / steps - t_sgd,
+           "note": "BASELINE config 4: fused allreduce+SGD inside each client every step, "
+                   "elastic update across counterpart pairs every tau steps"}
+    for grp in (W4, G4, D4, X4, C4):
+        grp.destroy()
+    if ccomm is not None:
+        ccomm.destroy()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -427,6 +470,9 @@ def main():
             grp.destroy()
         if lcomm is not comm:
             lcomm.destroy()
+        if p >= 2 and p % 2 == 0:
+            extra["config4"] = config4_sequence(args, p, rank, local, numels, dev, ecomm, cen,
+                                                stream, timed_calls)
         X.destroy()
         C.destroy()
         if ecomm is not comm:

@@ -240,7 +240,21 @@ def config4_sequence(args, p, rank, local, numels, dev, ecomm, cen, stream, time
            "easgd_amortised_us": t_seq / steps - t_sgd,
            "note": "BASELINE config 4: fused allreduce+SGD inside each client every step, "
                    "elastic update across counterpart pairs every tau steps"}
-    for grp in (W4, G4, D4, X4, C4):
+    extra_groups = []
+    if half == 1:
+        # one GPU per client: the elastic steps can use the fused tc_esgd_step (NEXT row f2)
+        G4e, D4e = tc.Group(ecomm, g4), tc.Group(ecomm, d4)
+        extra_groups = [G4e, D4e]
+
+        def fused():
+            for t in range(steps):
+                if t % tau == 0:
+                    tc.esgd_step(X4, C4, G4e, D4e, 0.1, stream=stream, **hp)
+                else:
+                    tc.sgd_step(W4, G4, D4, stream=stream, **hp)
+
+        out["mean_step_fused_us"] = timed_calls(fused) / steps
+    for grp in [W4, G4, D4, X4, C4] + extra_groups:
         grp.destroy()
     if ccomm is not None:
         ccomm.destroy()

@@ -396,6 +396,21 @@ def main():
         ta = max_over_ranks(e0.elapsed_time(e1) / K, world) / 1e3
         extra["allreduce_only"] = {"t_us": ta * 1e6, "busbw_gbs": S / ta / 1e9 * 2 * (p - 1) / p,
                                    "algo": comm.last_launch()[0]}
+        # tensor broadcast from rank 0 (weight initialisation): scatter + allgather
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                tc.broadcast(G, 0, stream=stream)
+            barrier(world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(K):
+                tc.broadcast(G, 0, stream=stream)
+            e1.record(stream)
+            stream.synchronize()
+        tb = max_over_ranks(e0.elapsed_time(e1) / K, world) / 1e3
+        extra["broadcast"] = {"t_us": tb * 1e6, "algbw_gbs": S / tb / 1e9,
+                              "busbw_gbs": S / tb / 1e9 * (p - 1) / p,
+                              "algo": comm.last_launch()[0]}
         if not args.no_nccl:
             import torch.distributed as dist
             flat = torch.empty(sum(numels), dtype=torch.float32, device="cuda")

@@ -269,6 +269,14 @@ TC_API tc_status tc_esgd_step(tc_group* x, tc_group* center, tc_group* g, tc_gro
                               float alpha, float lr, float momentum, float wd, float rescale,
                               void* stream);
 
+/* Tensor broadcast (MPI_Bcast of the weights at initialisation; the KVStore.pull
+ * broadcast): every rank's group := the root's group, bit for bit.  Scatter from
+ * the root (each rank copies its owner chunk of the root's tensors) then the allgather of the
+ * two-shot, so every GPU receives S bytes and the root sends S.  Collective; root identical on
+ * all ranks.  p = 1: no-op.  Errors: TC_ERR_INVALID_ARG (root outside [0, nranks)),
+ * TC_ERR_TIMEOUT, TC_ERR_BUSY, TC_ERR_CUDA. */
+TC_API tc_status tc_broadcast(tc_group* x, int root, void* stream);
+
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
  * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS,
  * 5 = low-latency, 6 = two-shot TMA), grid CTAs per rank, threads per CTA. */

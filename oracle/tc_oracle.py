@@ -24,6 +24,8 @@ Pins (tests/test_oracle_pins.py, -m "not gpu"):
                       alpha=0 identity; conservation; contraction; exact rational arithmetic.
   slot_partition   -- pinned: exact integer invariants (cover, disjoint, balance).
   esgd_sequence    -- composed of the three pinned parts (no closed form).
+  broadcast        -- the plain definition (copies of the root's group); pinned by rank
+                      identity and the root's group unchanged, bit for bit.
   esgd_step        -- NEXT row f2 (elastic then SGD with each client's own gradient): pinned by
                       exact rational evaluation on dyadic data and its special cases (alpha = 0
                       -> local sgd_step; lr = momentum = 0 -> easgd_update).
@@ -37,6 +39,7 @@ import numpy as np
 __all__ = [
     "allreduce", "allreduce_f64", "reduce_scatter", "allgather",
     "sgd_step", "sgd_step_f64", "easgd_update", "easgd_update_f64", "esgd_sequence", "esgd_step",
+    "broadcast",
     "slot_partition", "bus_bytes_per_rank", "predict_cost", "ring_allreduce_sim",
     "F", "R",
 ]
@@ -235,6 +238,14 @@ def easgd_update_f64(xs, center, alpha):
             s = s + d[i]
         c_out.append(xc + a * s)
     return x_out, c_out
+
+
+# ----------------------------------------------------------------------------------------
+# Tensor broadcast (MPI_Bcast of the weights at initialisation; KVStore.pull).
+# ----------------------------------------------------------------------------------------
+def broadcast(xs, root: int):
+    """Every rank's group becomes a copy of the root's (plain definition)."""
+    return [[np.array(a, dtype=np.float32, copy=True) for a in xs[root]] for _ in xs]
 
 
 # ----------------------------------------------------------------------------------------

@@ -70,6 +70,7 @@ constexpr int kT2Threads = 32 * (1 + kT2ConsumerWarps);
 // allgather the staged value (+ w, dw for SGD; + x, center for EASGD)
 // (ESGD, NEXT row f2: + w (= x), center, dw and the local gradient g)
 constexpr int t2_ops(int op, int p) {
+  if (op == 4) return 1;  // broadcast: the root's copy, then the owner's staged chunk
   const int rs = p + (op == 1 ? 2 : op == 2 ? 1 : op == 3 ? 3 : 0);
   const int ag = 1 + (op == 0 ? 0 : op == 3 ? 4 : 2);
   return rs > ag ? rs : ag;
@@ -83,7 +84,7 @@ constexpr int t2_smem(int op, int p) {
 }
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
-enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3 };
+enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4 };
 enum Algo {
   ALGO_LOCAL = 0,
   ALGO_TWOSHOT = 1,
@@ -157,6 +158,7 @@ struct KParams {
   int chunk_cap;         // slots per arena region (>= the largest owner chunk)
   DevState* state;       // [p] device-side call epochs (this process's ranks are valid)
   float scale, lr, mu, wd, rescale, alpha;
+  int root;              // broadcast root
   unsigned long long timeout_ns;
   int* err;              // host-mapped sticky error word
   int absent_rank;       // fault injection (emulated only), -1 off

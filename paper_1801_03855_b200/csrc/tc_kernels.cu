@@ -7,6 +7,7 @@ const void* kernel_ptr_allreduce(int algo, int p, int variant);
 const void* kernel_ptr_sgd(int algo, int p, int variant);
 const void* kernel_ptr_easgd(int algo, int p, int variant);
 const void* kernel_ptr_esgd(int algo, int p, int variant);
+const void* kernel_ptr_bcast(int algo, int p, int variant);
 
 namespace {
 const void* select_kernel(int op, int algo, int p, int variant) {
@@ -15,6 +16,7 @@ const void* select_kernel(int op, int algo, int p, int variant) {
     case OP_SGD: return kernel_ptr_sgd(algo, p, variant);
     case OP_EASGD: return kernel_ptr_easgd(algo, p, variant);
     case OP_ESGD: return kernel_ptr_esgd(algo, p, variant);
+    case OP_BCAST: return kernel_ptr_bcast(algo, p, variant);
   }
   return nullptr;
 }

@@ -191,7 +191,9 @@ __device__ __forceinline__ void sgd1(const KParams& kp, float G, float& w, float
 template <int OP, int PH, int P>
 __device__ __forceinline__ void elem(const KParams& kp, int r, const float* in, float& la,
                                      float& lb, float& lc) {
-  if constexpr (OP == OP_ALLREDUCE) {
+  if constexpr (OP == OP_BCAST) {
+    la = in[0];  // the root's value (reduce-scatter: the root's copy; allgather: the owner's)
+  } else if constexpr (OP == OP_ALLREDUCE) {
     if constexpr (PH == PH_RS) {
       double acc = (double)in[0];
 #pragma unroll
@@ -1179,6 +1181,8 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
                                         const float4* so, int ct, int nct) {
   using N = Needs<OP, PH, PH == PH_RS ? P : 2>;
   const size_t T = (size_t)kp.T;
+  // reduce-scatter sources: every rank's copy, or the root's alone (broadcast)
+  constexpr int NSRC = OP == OP_BCAST ? 1 : P;
   if (d.vec == 2) {
     // one partial slot from shared memory: valid lanes [lo_l, hi_l) are stored
     if (ct == 0) {
@@ -1186,18 +1190,18 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
       const int hi_l = (int)min((int64_t)4, kp.numel[d.t] - d.e);
       if constexpr (PH == PH_RS) {
         constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
-        float4 b = N::loadB ? so[P * V] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 c = N::loadC ? so[(P + NB) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 g = N::loadD ? so[(P + NB + NC) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 b = N::loadB ? so[NSRC * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 c = N::loadC ? so[(NSRC + NB) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 g = N::loadD ? so[(NSRC + NB + NC) * V] : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 oa = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
           if (l < lo_l || l >= hi_l) continue;
-          float in[P];
+          float in[NSRC];
 #pragma unroll
-          for (int q = 0; q < P; ++q) in[q] = lane_of(so[q * V], l);
+          for (int q = 0; q < NSRC; ++q) in[q] = lane_of(so[q * V], l);
           float la = 0.f, lb = lane_of(b, l), lc = lane_of(c, l);
-          elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g, l));
+          elem4<OP, PH_RS, NSRC>(kp, r, in, la, lb, lc, lane_of(g, l));
           lane(oa, l) = la;
           lane(b, l) = lb;
           if constexpr (N::storeA) st4(d.a + l, la);
@@ -1229,16 +1233,16 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
     for (int v0 = ct; v0 < d.n; v0 += nct * TU) {
       if constexpr (PH == PH_RS) {
         constexpr int NB = N::loadB ? 1 : 0, NC = N::loadC ? 1 : 0;
-        float4 x[TU][P], b[TU], c[TU], g[TU];
+        float4 x[TU][NSRC], b[TU], c[TU], g[TU];
 #pragma unroll
         for (int u = 0; u < TU; ++u) {
           const int v = v0 + u * nct;
           if (v < d.n) {
 #pragma unroll
-            for (int q = 0; q < P; ++q) x[u][q] = so[q * V + v];
-            b[u] = N::loadB ? so[P * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-            c[u] = N::loadC ? so[(P + NB) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-            g[u] = N::loadD ? so[(P + NB + NC) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < NSRC; ++q) x[u][q] = so[q * V + v];
+            b[u] = N::loadB ? so[NSRC * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            c[u] = N::loadC ? so[(NSRC + NB) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            g[u] = N::loadD ? so[(NSRC + NB + NC) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
 #pragma unroll
@@ -1248,11 +1252,11 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
           float4 oa;
 #pragma unroll
           for (int l = 0; l < 4; ++l) {
-            float in[P];
+            float in[NSRC];
 #pragma unroll
-            for (int q = 0; q < P; ++q) in[q] = lane_of(x[u][q], l);
+            for (int q = 0; q < NSRC; ++q) in[q] = lane_of(x[u][q], l);
             float la = 0.f, lb = lane_of(b[u], l), lc = lane_of(c[u], l);
-            elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, lane_of(g[u], l));
+            elem4<OP, PH_RS, NSRC>(kp, r, in, la, lb, lc, lane_of(g[u], l));
             lane(oa, l) = la;
             lane(b[u], l) = lb;
             lane(c[u], l) = lc;
@@ -1302,11 +1306,12 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
     const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
     for (int64_t j = j0 + ct; j < j1; j += nct) {
       if constexpr (PH == PH_RS) {
-        float in[P];
+        float in[NSRC];
 #pragma unroll
-        for (int q = 0; q < P; ++q) in[q] = ld4(kp.a[q * T + d.t] + d.e + j);
+        for (int q = 0; q < NSRC; ++q)
+          in[q] = ld4(kp.a[(OP == OP_BCAST ? kp.root : q) * T + d.t] + d.e + j);
         float la = 0.f, lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
-        elem4<OP, PH_RS, P>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
+        elem4<OP, PH_RS, NSRC>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
         if constexpr (N::storeA) st4(d.a + j, la);
         if constexpr (N::storeB) st4(d.b + j, lb);
         if constexpr (N::storeC) st4(d.c + j, lc);
@@ -1365,8 +1370,12 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
         bool vec = !part || d.n == 1;
         int o = 0;
         if constexpr (PH == PH_RS) {
+          if constexpr (OP == OP_BCAST) {
+            src[o++] = kp.a[(size_t)kp.root * T + d.t] + d.e;
+          } else {
 #pragma unroll
-          for (int q = 0; q < P; ++q) src[o++] = kp.a[q * T + d.t] + d.e;
+            for (int q = 0; q < P; ++q) src[o++] = kp.a[q * T + d.t] + d.e;
+          }
         } else {
           src[o++] = d.st;
           if constexpr (N::loadA) src[o++] = d.a;
@@ -1446,7 +1455,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
   using NR = Needs<OP, PH_RS, P>;
   using NG = Needs<OP, PH_AG, 2>;
   constexpr int OPS = t2_ops(OP, P), NS = t2_stages(OP, P);
-  constexpr int OPS_RS = P + NR::loadB + NR::loadC + NR::loadD;
+  constexpr int OPS_RS = (OP == OP_BCAST ? 1 : P) + NR::loadB + NR::loadC + NR::loadD;
   constexpr int OPS_AG = 1 + NG::loadA + NG::loadB + NG::loadC + NG::loadD;
   constexpr int G_RS = t2_pack(OPS / OPS_RS), G_AG = t2_pack(OPS / OPS_AG);
   static_assert(OPS_RS <= OPS && OPS_AG <= OPS, "stage too small");

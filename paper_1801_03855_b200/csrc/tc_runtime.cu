@@ -329,7 +329,7 @@ tc_status grow_arena(Comm& c, int64_t need) {
 // ------------------------------------------------------------------ hot-path dispatcher
 tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr, float mu,
                   float wd, float rescale, float alpha, cudaStream_t stream,
-                  Group* gd = nullptr) {
+                  Group* gd = nullptr, int root = 0) {
   Comm& c = *ga->comm;
   BusyGuard busy(c.busy);
   if (!busy.ok) return TC_ERR_BUSY;
@@ -352,6 +352,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.b = gb ? gb->d_ptrs : nullptr;
   kp.c = gc ? gc->d_ptrs : nullptr;
   kp.d = gd ? gd->d_ptrs : nullptr;
+  kp.root = root;
   kp.mc = ga->d_mc;
   kp.flags = c.d_flags;
   kp.stage = c.d_stage;
@@ -381,6 +382,9 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   const int variant = op == OP_ESGD ? 0 : c.variant;
   if (p == 1) {
     algo = ALGO_LOCAL;
+  } else if (op == OP_BCAST) {  // implemented by the TMA two-shot only
+    algo = ALGO_TWOSHOT_TMA;
+    if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   } else if (op == OP_ESGD) {
     algo = c.algo_override == ALGO_TWOSHOT_BAL ? ALGO_TWOSHOT_BAL : ALGO_TWOSHOT_TMA;
     if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
@@ -921,6 +925,13 @@ tc_status tc_esgd_step(tc_group* x, tc_group* center, tc_group* g, tc_group* dw,
     return TC_ERR_SHAPE_MISMATCH;
   return run_hot(OP_ESGD, &x->g, &center->g, &dw->g, 1.0f, lr, momentum, wd, rescale, alpha,
                  (cudaStream_t)stream, &g->g);
+}
+
+tc_status tc_broadcast(tc_group* x, int root, void* stream) {
+  if (!x || root < 0 || root >= x->g.comm->nranks) return TC_ERR_INVALID_ARG;
+  if (x->g.comm->nranks == 1) return TC_OK;  // the root's tensors are the result
+  return run_hot(OP_BCAST, &x->g, nullptr, nullptr, 1.0f, 0, 0, 0, 0, 0, (cudaStream_t)stream,
+                 nullptr, root);
 }
 
 tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream) {

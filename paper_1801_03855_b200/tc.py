@@ -75,6 +75,7 @@ _SIGS = {
     "tc_allreduce": (_c_int, [_vp, _c_float, _vp]),
     "tc_sgd_step": (_c_int, [_vp, _vp, _vp, _c_float, _c_float, _c_float, _c_float, _vp]),
     "tc_easgd_update": (_c_int, [_vp, _vp, _c_float, _vp]),
+    "tc_broadcast": (_c_int, [_vp, _c_int, _vp]),
     "tc_esgd_step": (_c_int, [_vp, _vp, _vp, _vp, _c_float, _c_float, _c_float, _c_float,
                               _c_float, _vp]),
 }
@@ -385,6 +386,11 @@ def sgd_step(w: Group, g: Group, dw: Group, lr: float, momentum: float = 0.0, wd
 def easgd_update(x: Group, center: Group, alpha: float, stream=None):
     _check(LIB.tc_easgd_update(x.h, center.h, float(alpha), _stream_ptr(stream)),
            "tc_easgd_update")
+
+
+def broadcast(x: Group, root: int = 0, stream=None):
+    """Every rank's group := the root's (weight initialisation)."""
+    _check(LIB.tc_broadcast(x.h, int(root), _stream_ptr(stream)), "tc_broadcast")
 
 
 def esgd_step(x: Group, center: Group, g: Group, dw: Group, alpha: float, lr: float,

@@ -82,6 +82,15 @@ def main():
     assert st == tc.tc.TC_ERR_NOT_SHAREABLE, st
     assert not out.value
 
+    # tensor broadcast from the last rank
+    numels = [7, 13, 1000, 0, 50001]
+    xs = [W.group(numels, "grad", 64, 0, k, W.GRAD) for k in range(p)]
+    dev = to_dev(xs[rank])
+    with tc.Group(comm, dev) as g:
+        tc.broadcast(g, p - 1)
+        assert_bitwise(to_host(dev), O.broadcast(xs, p - 1)[rank], "broadcast")
+    assert comm.async_error() == 0
+
     # NEXT row f2: fused elastic + SGD with each rank's own gradient (one GPU per client)
     comm.set_tuning(0, 0, -1)
     comm.set_ll_max(-1)

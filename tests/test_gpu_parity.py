@@ -494,3 +494,26 @@ def test_esgd_step_errors():
     ga.destroy()
     gb.destroy()
     comm.destroy()
+
+
+# ------------------------------------------------------------------ tensor broadcast
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_broadcast(p, offset):
+    numels = [7, 13, 1000, 4096, 0, 2, 3001, 9000]
+    xs = [W.group(numels, "grad", 84, 0, k, W.GRAD) for k in range(p)]
+    for root in sorted({0, p - 1}):
+        comm = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
+        dev = [to_dev(x, offset=offset) for x in xs]
+        g = tc.Group(comm, dev if p > 1 else dev[0])
+        tc.broadcast(g, root)
+        if p > 1:
+            assert comm.last_launch()[0] == "two-shot-tma"
+        want = O.broadcast(xs, root)
+        for r in range(p):
+            assert_bitwise(to_host(dev[r]), want[r], f"rank {r} root {root}")
+        assert comm.async_error() == 0
+        with pytest.raises(tc.TcError):
+            tc.broadcast(g, p)  # root outside the comm
+        g.destroy()
+        comm.destroy()

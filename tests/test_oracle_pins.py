@@ -419,3 +419,15 @@ def test_esgd_step_special_cases():
         assert np.array_equal(xc[t], ce[t])
         for i in range(c):
             assert np.array_equal(x[i][t], xe[i][t]) and not dw[i][t].any()
+
+
+# ------------------------------------------------------------------ tensor broadcast
+def test_broadcast_definition():
+    numels = [7, 13, 0, 1000]
+    xs = [W.group(numels, "grad", 83, 0, k, W.GRAD) for k in range(4)]
+    for root in range(4):
+        out = O.broadcast(xs, root)
+        for r in range(4):
+            for t in range(len(numels)):
+                assert out[r][t].tobytes() == xs[root][t].tobytes()
+                assert out[r][t] is not xs[root][t]

@@ -151,9 +151,10 @@ TC_API tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes);
  * the switch in fp32 (order unspecified): exact for integer-valued data, else within
  * (p-1) ulp-scale of the float64 sum; identical on every rank.  6 = two-shot pull with the
  * data moved by TMA bulk copies through a shared-memory stage ring (one CTA per SM at most;
- * tc_comm_set_tuning's num_ctas sets how many SMs it occupies -- few CTAs still move data at
- * link speed, leaving the rest of the GPU to concurrent work); bit-identical to 1 and 3.
- * Automatic: pull, except tc_allreduce of eligible groups at p >= 6 -> NVLS.
+ * tc_comm_set_tuning's num_ctas sets how many SMs it occupies); 7 = the same with tiles
+ * claimed from per-rank counters instead of dealt round-robin.  1, 3, 6 and 7 give
+ * bit-identical results.  Automatic (0): low-latency / one-shot for small groups, 6 above
+ * (measured fastest), except tc_allreduce of multicast-eligible groups at p >= 6 -> NVLS.
  * Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 
@@ -279,7 +280,8 @@ TC_API tc_status tc_broadcast(tc_group* x, int root, void* stream);
 
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
  * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS,
- * 5 = low-latency, 6 = two-shot TMA), grid CTAs per rank, threads per CTA. */
+ * 5 = low-latency, 6 = two-shot TMA, 7 = two-shot TMA with claimed tiles), grid CTAs per
+ * rank, threads per CTA. */
 TC_API tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads);
 
 #ifdef __cplusplus

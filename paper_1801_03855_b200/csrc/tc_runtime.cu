@@ -455,6 +455,10 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * occ);
   } else if (twoshot && c.tune_ctas > 0) {
     ctas = c.tune_ctas;
+  } else if (algo == ALGO_NVLS && op == OP_ALLREDUCE) {
+    // switch reductions saturate with ~half the SMs (p = 4 allreduce: 74 CTAs 285 us,
+    // 148 x 512 299, 296 x 512 307); the SGD epilogue pass wants the full grid (392 vs 470 us)
+    ctas = (int)std::min<int64_t>(want, c.num_sms / 2);
   } else {
     ctas = (int)std::min<int64_t>(
         want, (int64_t)c.num_sms * ((algo == ALGO_ONESHOT || algo == ALGO_LL) ? 1 : occ));

@@ -264,7 +264,7 @@ def config4_sequence(args, p, rank, local, numels, dev, ecomm, cen, stream, time
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="tc", choices=["tc", "reference"])
     ap.add_argument("--config", default="resnet50", choices=["resnet50", "alexnet", "vgg16"])

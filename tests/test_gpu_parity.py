@@ -406,9 +406,10 @@ def _sampled_check(numels, outs, xs, scale, p, seed=0, per_tensor=48):
 
 @pytest.mark.parametrize("group,p,oneshot", [("resnet50", 1, -1), ("resnet50", 2, TWOSHOT),
                                              ("resnet50", 4, PUSH), ("alexnet", 2, TWOSHOT),
-                                             ("resnet50", 4, TMA), ("resnet50", 4, BAL)])
+                                             ("resnet50", 4, TMA), ("resnet50", 4, BAL),
+                                             ("vgg16", 2, TMA)])
 def test_full_size_groups_sampled(group, p, oneshot):
-    """Configs 2/3 at their full size (ResNet-50 25.6M, AlexNet 61.1M fp32 per rank), in the
+    """Configs 2/3 at their full size (ResNet-50 25.6M, AlexNet 61.1M, VGG-16 138.4M fp32 per rank), in the
     launch configuration bench.py times, checked on sampled outputs."""
     numels = W.GROUPS[group]
     xs = [W.group(numels, "grad", W.CFG_ALEX_VGG if group != "resnet50" else W.CFG_RESNET50, 0,

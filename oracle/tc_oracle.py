@@ -29,8 +29,10 @@ Pins (tests/test_oracle_pins.py, -m "not gpu"):
   esgd_step        -- NEXT row f2 (elastic then SGD with each client's own gradient): pinned by
                       exact rational evaluation on dyadic data and its special cases (alpha = 0
                       -> local sgd_step; lr = momentum = 0 -> easgd_update).
-  The momentum term (mu != 0) follows reading R12; the paper fixes no formula for it, so for
-  that term alone: parity unpinned (to the paper) -- only to R12's own closed form.
+  The momentum term (mu != 0) follows reading R12; the paper fixes no formula for it (P:158 names
+  "momentum SGD" only), so it is pinned to its own closed form and to an independent library
+  routine for the standard heavy-ball form (torch.optim.SGD, float64, several steps:
+  tests/test_oracle_pins.py::test_sgd_momentum_matches_library_optimizer).
 """
 from __future__ import annotations
 

@@ -221,6 +221,31 @@ def test_sgd_momentum_geometric_series():
     assert Fraction(float(dw[0][0])) == -Fraction(lr) * Fraction(rs) * 8 * (1 - Fraction(mu) ** K) / (1 - Fraction(mu))
 
 
+def test_sgd_momentum_matches_library_optimizer():
+    """R12's momentum form (P:158 names "momentum SGD") against an independent library routine:
+    torch.optim.SGD (buf <- mu*buf + g + wd*w; w <- w - lr*buf, dampening 0) is the same
+    trajectory for constant lr with dw = -lr*buf.  Several steps, p = 3 ranks, float64; the
+    gradient the optimiser sees is rescale * (the plain sum over ranks)."""
+    import torch
+    p, n, steps = 3, 257, 5
+    lr, mu, wd, rs = 0.125, 0.875, 0.0078125, 0.25  # exact in fp32 (they cross a C float)
+    w = W.group([n], "param", 61, 0, 0, W.PARAM)
+    dw = [np.zeros(n, np.float32)]
+    tw = torch.tensor(w[0].astype(np.float64), requires_grad=True)
+    opt = torch.optim.SGD([tw], lr=lr, momentum=mu, weight_decay=wd, dampening=0.0)
+    ws_o, dws_o = [w] * p, [dw] * p
+    for s in range(steps):
+        gs = [W.group([n], "grad", 61, s, k, W.GRAD) for k in range(p)]
+        _, ws_o, dws_o = O.sgd_step_f64(ws_o, gs, dws_o, lr, mu, wd, rs)
+        tw.grad = torch.tensor(rs * np.stack([g[0].astype(np.float64) for g in gs]).sum(0))
+        opt.step()
+    ref = tw.detach().numpy()
+    for k in range(p):
+        np.testing.assert_allclose(ws_o[k][0], ref, rtol=1e-12, atol=1e-15)
+    buf = opt.state[tw]["momentum_buffer"].numpy()
+    np.testing.assert_allclose(dws_o[0][0], -lr * buf, rtol=1e-12, atol=1e-15)
+
+
 def test_sgd_zero_grad_identity():
     w = W.group([33], "param", 89, 0, 0, W.PARAM)
     z = [np.zeros(33, np.float32)]

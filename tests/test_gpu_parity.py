@@ -503,7 +503,7 @@ def test_esgd_step_errors():
 def test_broadcast(p, offset):
     numels = [7, 13, 1000, 4096, 0, 2, 3001, 9000]
     xs = [W.group(numels, "grad", 84, 0, k, W.GRAD) for k in range(p)]
-    for root in sorted({0, p - 1}):
+    for root in sorted({0, p // 2, p - 1}):  # p >= 3: the root owns no chunk (first/middle/last)
         comm = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
         dev = [to_dev(x, offset=offset) for x in xs]
         g = tc.Group(comm, dev if p > 1 else dev[0])

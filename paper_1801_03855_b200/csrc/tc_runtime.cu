@@ -391,10 +391,12 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   } else {
     // One-shot moves (p-1)S per GPU against 2(p-1)/p S for two-shot but needs one barrier
     // less.  Measured crossover against the TMA two-shot (config-5 sweep): p = 2 one-shot
-    // 22-23 us at 4 MiB (TMA 24-35), two-shot from 16 MiB; p = 4 even at 4 MiB (34-36 vs 29-37
-    // us), TMA ahead above.
+    // 22-23 us at 4 MiB (TMA 24-35), two-shot from 16 MiB; p = 3 ties at 4 MiB (27.1-28.4 vs
+    // 27.5-32.1 us); p = 4 ties at 2 MiB (24.4-25.4 vs 24.7-25.5) and loses at 4 MiB (33.6-35.2
+    // vs TMA 28.3-33.3 for 1..1024 tensors, profiles/r01_oneshot_limit_p4.jsonl).
     const int64_t auto_lim = p == 2 ? (int64_t)kStageCapacity
-                           : p <= 4 ? (int64_t)kStageCapacity / 2 : kDefaultOneshotMax;
+                           : p == 3 ? (int64_t)kStageCapacity / 2
+                           : p == 4 ? (int64_t)kStageCapacity / 4 : kDefaultOneshotMax;
     int64_t lim = c.tune_oneshot < 0 ? auto_lim : c.tune_oneshot;
     if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
     // Automatic choice (measured on B200, config-5 sweep and ResNet-50 group):

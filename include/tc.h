@@ -131,7 +131,8 @@ TC_API tc_status tc_comm_create_emulated(int nranks, int cuda_device, tc_comm** 
 /* Launch tuning, must be identical on all ranks.  num_ctas: CTAs per rank for two-shot calls
  * (0 = automatic: a full wave of the GPU); threads: threads per CTA (0 = 512; a multiple of 32
  * in [64, 1024]); oneshot_max_bytes: groups of at most this many bytes use the one-shot
- * algorithm (-1 = automatic, 0 = never; capped by the staging capacity).  Applies to later
+ * algorithm (-1 = automatic: 8 MiB at p = 2, 4 MiB at p = 3, 2 MiB at p = 4, 256 KiB beyond;
+ * 0 = never; capped by the staging capacity).  Applies to later
  * calls.  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t oneshot_max_bytes);
 

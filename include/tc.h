@@ -149,18 +149,32 @@ TC_API tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes);
  * (stores into the owners' receive scratch), 4 = NVLS (switch reduction, multimem.ld_reduce +
  * multimem.st; only for groups in tc_mem_alloc memory, else two-shot).  1 and 3 end with the
  * staged pull allgather and give bit-identical results (float64, rank order).  NVLS sums in
- * the switch in fp32 (order unspecified): exact for integer-valued data, else within
- * (p-1) ulp-scale of the float64 sum; identical on every rank.  6 = two-shot pull with the
- * data moved by TMA bulk copies through a shared-memory stage ring (one CTA per SM at most;
- * tc_comm_set_tuning's num_ctas sets how many SMs it occupies); 7 = the same with tiles
- * claimed from per-rank counters instead of dealt round-robin.  1, 3, 6 and 7 give
- * bit-identical results.  Automatic (0): low-latency / one-shot for small groups, 6 above
- * (measured fastest), except tc_allreduce of multicast-eligible groups at p >= 6 -> NVLS.
+ * the switch in fp32 (order unspecified): exact for integer-valued data, else within the
+ * BASELINE tolerance 1e-5 * sum_k |x_k| of the float64 sum; identical on every rank.  6 =
+ * two-shot pull with the data moved by TMA bulk copies through a shared-memory stage ring (one
+ * CTA per SM at most; tc_comm_set_tuning's num_ctas sets how many SMs it occupies); 7 = the
+ * same with tiles claimed from per-rank counters instead of dealt round-robin.  1, 3, 6 and 7
+ * give bit-identical results.  Automatic (0): low-latency / one-shot for small groups, 6 above
+ * (measured fastest); NVLS only when tc_comm_set_switch_reduction(comm, 1) allowed it.
  * Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 
+/* Whether the AUTOMATIC choice may use the NVSwitch reduction (algorithm 4) for groups in
+ * tc_mem_alloc memory (must be identical on all ranks).  0 (default): never -- every automatic
+ * result is bit-identical to the float64 rank-order oracle.  1: allowed where it moves fewer
+ * bytes per GPU than the two-shot ((1 + 1/p) S against 2(p-1)/p S, p >= 6 with the p = 4
+ * measured rates) -- results then follow algorithm 4's tolerance contract.
+ * Errors: TC_ERR_INVALID_ARG (allow not 0 or 1). */
+TC_API tc_status tc_comm_set_switch_reduction(tc_comm* comm, int allow);
+
 /* Device-barrier timeout in milliseconds (default 30000, or env TC_TIMEOUT_MS). */
 TC_API tc_status tc_comm_set_timeout(tc_comm* comm, int64_t timeout_ms);
+
+/* Fault injection for tests: while hold != 0 the comm is marked busy exactly as if another
+ * host thread were inside a call on it, so every call that takes the comm (hot path, group
+ * create/destroy) returns TC_ERR_BUSY ("one collective call per communicator at a
+ * time").  Not collective. */
+TC_API tc_status tc_comm_set_debug_busy(tc_comm* comm, int hold);
 
 /* Fault injection for tests (emulated comms only): the CTAs of rank `absent_rank` return
  * immediately without arriving at any barrier (-1 = off), so the other ranks time out. */
@@ -196,6 +210,8 @@ TC_API tc_status tc_comm_destroy(tc_comm* comm);
  * tc_comm_destroy.  Errors: TC_ERR_INVALID_ARG, TC_ERR_UNSUPPORTED (emulated comm or no VMM
  * driver entry points), TC_ERR_CUDA, TC_ERR_BOOTSTRAP. */
 TC_API tc_status tc_mem_alloc(tc_comm* comm, size_t bytes, void** ptr);
+/* Collective.  `ptr` must be a pointer tc_mem_alloc returned.  TC_ERR_INVALID_ARG if it is not,
+ * or while a live group still has tensors in the allocation (destroy those groups first). */
 TC_API tc_status tc_mem_free(tc_comm* comm, void* ptr);
 /* 1 if this comm's device supports NVSwitch multicast + reduction, else 0. */
 TC_API int tc_comm_multicast_supported(const tc_comm* comm);
@@ -215,12 +231,18 @@ TC_API int tc_comm_multicast_supported(const tc_comm* comm);
  * the same allocation for every CUDA allocator (bases 256-B aligned, sizes rounded up).
  * Errors: TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH (ranks disagree on T or any n_t; returned
  * on every rank), TC_ERR_NOT_SHAREABLE (e.g. PyTorch expandable_segments allocations),
- * TC_ERR_CUDA, TC_ERR_BOOTSTRAP. */
+ * TC_ERR_BUSY (another call on the comm is in progress), TC_ERR_CUDA, TC_ERR_BOOTSTRAP. */
 TC_API tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const int64_t* numels,
                           tc_group** out);
 
 /* Collective: synchronizes the device, waits for every rank, then unmaps. */
 TC_API tc_status tc_group_destroy(tc_group* group);
+
+/* CTA budget of this group's hot-path launches (0 = the comm's tc_comm_set_tuning value), so
+ * e.g. the buckets of an overlapped step can run on a few SMs without changing the comm's
+ * state for other groups.  Must be identical on all ranks (the per-CTA barriers pair CTA b of
+ * every rank).  Not collective.  Errors: TC_ERR_INVALID_ARG (num_ctas outside [0, 1024]). */
+TC_API tc_status tc_group_set_num_ctas(tc_group* group, int num_ctas);
 
 /* ---------------------------------------------------------------------------------------
  * Hot path.  One kernel launch per call on `stream`.
@@ -229,7 +251,8 @@ TC_API tc_status tc_group_destroy(tc_group* group);
 /* A3+A4 (or A5 one-shot for small groups): in place, on every rank,
  *     x[t][j] := round_fp32( (sum_{k=0..p-1} x_k[t][j]) * scale )
  * summed in float64 in canonical rank order k = 0..p-1 and rounded once (readings R3, R4), so
- * the result is bit-identical on every rank and for every algorithm.  Errors:
+ * the result is bit-identical on every rank and for every P2P algorithm (NVLS, algorithm 4:
+ * see tc_comm_set_algorithm).  Errors:
  * TC_ERR_INVALID_ARG (NULL group, non-finite scale), TC_ERR_TIMEOUT (sticky), TC_ERR_BUSY,
  * TC_ERR_CUDA (launch failure). */
 TC_API tc_status tc_allreduce(tc_group* x, float scale, void* stream);

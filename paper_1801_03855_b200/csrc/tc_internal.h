@@ -111,6 +111,7 @@ struct Plan {
 
 struct Comm;
 int find_sym(const Comm& c, const void* p, size_t bytes, int64_t* offset);
+void sym_ref(Comm& c, const void* base, int delta);
 bool multicast_supported(int device);
 void free_all_sym(Comm& c);
 
@@ -163,18 +164,17 @@ struct KParams {
   int* err;              // host-mapped sticky error word
   int absent_rank;       // fault injection (emulated only), -1 off
   unsigned long long* prof; // optional per-CTA phase timestamps [nlocal*ctas][8] (ns)
-  const int4* tiles;     // p = 1 TMA stream: {tensor, first element, elements, 0} per tile
+  const int4* tiles;     // p = 1 TMA stream: {tensor, first element lo32, elements, first element hi32}
   int ntiles;
   const int4* tiles2;    // p >= 2 TMA two-shot: {tensor, first slot, slots, 0} per tile,
   int tile2_off[kMaxRanks + 1];  // owner q's tiles: [tile2_off[q], tile2_off[q + 1])
 };
 
 // Kernel launchers (tc_kernels.cu).
-// `variant` selects an alternative launch shape for experiments (env TC_VARIANT; 0 = default).
 cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int threads, int nlocal,
-                       bool cooperative, cudaStream_t stream, int variant);
-int max_ctas_per_sm(int op, int algo, int p, int threads, int variant);
-int launch_threads(int op, int algo, int p, int threads, int variant);
+                       bool cooperative, cudaStream_t stream);
+int max_ctas_per_sm(int op, int algo, int p, int threads);
+int launch_threads(int op, int algo, int p, int threads);
 
 // ---------------------------------------------------------------- runtime objects
 // One symmetric allocation (tc_mem_alloc): every rank's physical memory mapped locally (uc[r]),
@@ -187,6 +187,7 @@ struct SymAlloc {
   void* uc[kMaxRanks] = {};
   uint64_t mc_handle = 0;
   void* mc = nullptr;
+  int refs = 0;          // live groups with tensors in this allocation (tc_mem_free refuses)
 };
 
 struct MappedBase {
@@ -215,7 +216,7 @@ struct Comm {
   int64_t arena_cap = 0;          // slots per region
   std::vector<std::pair<int, std::string>> arena_keys;  // peer arena mappings held
   int algo_override = 0;          // 0 auto, else an Algo
-  int variant = 0;                // launch-shape experiment (env TC_VARIANT)
+  bool allow_switch = false;      // automatic choice may use NVLS (fp32 sums in the switch)
   int tune_ctas = 0, tune_threads = 512;
   int64_t tune_oneshot = -1;
   int64_t tune_ll = -1;
@@ -251,6 +252,8 @@ struct Group {
   int ntiles = 0;
   int4* d_tiles2 = nullptr;      // p >= 2: owner-chunk tiles of the TMA two-shot
   std::vector<int> tile2_off;    // [p + 1]
+  std::vector<void*> sym_bases;  // symmetric allocations (this rank's base) the group uses
+  int num_ctas = 0;              // per-group CTA budget (0 = the comm's tuning)
 };
 
 }  // namespace tc

@@ -3,32 +3,32 @@
 #include "tc_internal.h"
 
 namespace tc {
-const void* kernel_ptr_allreduce(int algo, int p, int variant);
-const void* kernel_ptr_sgd(int algo, int p, int variant);
-const void* kernel_ptr_easgd(int algo, int p, int variant);
-const void* kernel_ptr_esgd(int algo, int p, int variant);
-const void* kernel_ptr_bcast(int algo, int p, int variant);
+const void* kernel_ptr_allreduce(int algo, int p);
+const void* kernel_ptr_sgd(int algo, int p);
+const void* kernel_ptr_easgd(int algo, int p);
+const void* kernel_ptr_esgd(int algo, int p);
+const void* kernel_ptr_bcast(int algo, int p);
 
 namespace {
-const void* select_kernel(int op, int algo, int p, int variant) {
+const void* select_kernel(int op, int algo, int p) {
   switch (op) {
-    case OP_ALLREDUCE: return kernel_ptr_allreduce(algo, p, variant);
-    case OP_SGD: return kernel_ptr_sgd(algo, p, variant);
-    case OP_EASGD: return kernel_ptr_easgd(algo, p, variant);
-    case OP_ESGD: return kernel_ptr_esgd(algo, p, variant);
-    case OP_BCAST: return kernel_ptr_bcast(algo, p, variant);
+    case OP_ALLREDUCE: return kernel_ptr_allreduce(algo, p);
+    case OP_SGD: return kernel_ptr_sgd(algo, p);
+    case OP_EASGD: return kernel_ptr_easgd(algo, p);
+    case OP_ESGD: return kernel_ptr_esgd(algo, p);
+    case OP_BCAST: return kernel_ptr_bcast(algo, p);
   }
   return nullptr;
 }
 
-// TMA kernels run fixed thread counts with dynamic shared memory: the p = 1 stream (variant 0
-// of ALGO_LOCAL) and the TMA two-shot.
+// TMA kernels run fixed thread counts with dynamic shared memory: the p = 1 stream (ALGO_LOCAL)
+// and the TMA two-shot.
 struct Shape {
   int threads;
   int smem;
 };
-Shape shape_of(int op, int algo, int p, int threads, int variant) {
-  if (algo == ALGO_LOCAL && variant == 0)
+Shape shape_of(int op, int algo, int p, int threads) {
+  if (algo == ALGO_LOCAL)
     return {kTmaThreads, op == OP_ESGD ? kTmaSmem4 : kTmaSmem};
   if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL) return {kT2Threads, t2_smem(op, p)};
   return {threads, 0};
@@ -41,9 +41,9 @@ cudaError_t prepare(const void* k, const Shape& sh) {
 
 }  // namespace
 
-int max_ctas_per_sm(int op, int algo, int p, int threads, int variant) {
-  const void* k = select_kernel(op, algo, p, variant);
-  const Shape sh = shape_of(op, algo, p, threads, variant);
+int max_ctas_per_sm(int op, int algo, int p, int threads) {
+  const void* k = select_kernel(op, algo, p);
+  const Shape sh = shape_of(op, algo, p, threads);
   if (!k || prepare(k, sh) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, sh.threads, sh.smem) != cudaSuccess)
@@ -51,15 +51,15 @@ int max_ctas_per_sm(int op, int algo, int p, int threads, int variant) {
   return n;
 }
 
-int launch_threads(int op, int algo, int p, int threads, int variant) {
-  return shape_of(op, algo, p, threads, variant).threads;
+int launch_threads(int op, int algo, int p, int threads) {
+  return shape_of(op, algo, p, threads).threads;
 }
 
 cudaError_t launch_hot(int op, int algo, const KParams& kp, int ctas, int threads, int nlocal,
-                       bool cooperative, cudaStream_t stream, int variant) {
-  const void* k = select_kernel(op, algo, kp.p, variant);
+                       bool cooperative, cudaStream_t stream) {
+  const void* k = select_kernel(op, algo, kp.p);
   if (!k) return cudaErrorInvalidValue;
-  const Shape sh = shape_of(op, algo, kp.p, threads, variant);
+  const Shape sh = shape_of(op, algo, kp.p, threads);
   cudaError_t e = prepare(k, sh);
   if (e != cudaSuccess) return e;
   KParams arg = kp;

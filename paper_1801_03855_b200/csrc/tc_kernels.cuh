@@ -929,93 +929,6 @@ __global__ void __launch_bounds__(512, MINB) k_nvls(KParams kp) {
   stamp(kp, 5);
 }
 
-template <int OP, int MINB, int U>
-__global__ void __launch_bounds__(512, MINB) k_local(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  ReduceBody<OP, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
-  slot_loop<U>(kp, 0, kp.M, body);
-}
-
-// p = 1, lean variant: a piece (128 slots) that lies inside one tensor and is made of full,
-// aligned 16-B slots -- almost every piece of a real gradient group -- is streamed with
-// warp-uniform affine addresses (no per-slot lookup, few registers); only pieces that straddle a
-// tensor boundary or hold a partial/unaligned slot take the generic per-slot path.
-template <int OP, int U>
-__device__ __forceinline__ void local_fast_piece(const KParams& kp, int r, float* pa, float* pb,
-                                                 float* pc, int ln, int nslots) {
-  using N = Needs<OP, PH_RS, 1>;
-#pragma unroll 1
-  for (int base = 0; base < nslots; base += 32 * U) {
-    float4 va[U], vb[U], vc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + ln + 32 * u;
-      if (i < nslots) {
-        va[u] = ld16(pa + 4 * (size_t)i);
-        if constexpr (N::loadB) vb[u] = ld16(pb + 4 * (size_t)i);
-        if constexpr (N::loadC) vc[u] = ld16(pc + 4 * (size_t)i);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + ln + 32 * u;
-      if (i < nslots) {
-        float4 oa;
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          const float in[1] = {lane_of(va[u], l)};
-          float la = 0.f;
-          float lb = N::loadB ? lane_of(vb[u], l) : 0.f;
-          float lc = N::loadC ? lane_of(vc[u], l) : 0.f;
-          elem<OP, PH_RS, 1>(kp, r, in, la, lb, lc);
-          lane(oa, l) = la;
-          if constexpr (N::storeB) lane(vb[u], l) = lb;
-          if constexpr (N::storeC) lane(vc[u], l) = lc;
-        }
-        if constexpr (N::storeA) st16(pa + 4 * (size_t)i, oa);
-        if constexpr (N::storeB) st16(pb + 4 * (size_t)i, vb[u]);
-        if constexpr (N::storeC) st16(pc + 4 * (size_t)i, vc[u]);
-      }
-    }
-  }
-}
-
-template <int OP, int MINB, int U>
-__global__ void __launch_bounds__(512, MINB) k_local_lean(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  const int lane_id = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int M = kp.M;
-  const int npieces = (M + kPiece - 1) / kPiece;
-  ReduceBody<OP, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
-  TensorCache<ReduceBody<OP, 1, SRC_TENSORS, false>::NP> tc;
-  tc.t = -1;
-  tc.lo = tc.hi = 0;
-  for (int c = blockIdx.x + gridDim.x * warp; c < npieces; c += gridDim.x * nw) {
-    const int pbase = c * kPiece;
-    const int pend = min(M, pbase + kPiece);
-    SlotRef r0;
-    resolve(kp, body, tc, pbase, r0);  // warp-uniform: every lane resolves the same slot
-    if (tc.vec && r0.e >= 0 && pend <= tc.hi && (int64_t)(pend - tc.lo) * 4 - tc.shift <= tc.n) {
-      local_fast_piece<OP, U>(kp, r, tc.ptr[0] + r0.e, tc.ptr[1] ? tc.ptr[1] + r0.e : nullptr,
-                              tc.ptr[2] ? tc.ptr[2] + r0.e : nullptr, lane_id, pend - pbase);
-      continue;
-    }
-#pragma unroll 1
-    for (int s = pbase + lane_id; s < pend; s += 32) {
-      SlotRef ref;
-      typename ReduceBody<OP, 1, SRC_TENSORS, false>::State st;
-      resolve(kp, body, tc, s, ref);
-      if (ref.vec) {
-        body.template load<true>(ref, tc.ptr, st);
-        body.template finish<true>(ref, st);
-      } else {
-        body.template load<false>(ref, tc.ptr, st);
-        body.template finish<false>(ref, st);
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------------ p = 1: TMA stream
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -1026,6 +939,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!P bra W_%=;\n}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+
+// First element of a p = 1 tile: 64-bit, split over the .y (low) and .w (high) words, so tensors
+// of 2^31 elements or more (8 GiB of fp32) are addressed correctly.
+__device__ __forceinline__ int64_t tile_elem(const int4& tl) {
+  return (int64_t)(uint32_t)tl.y | ((int64_t)tl.w << 32);
 }
 
 // p = 1 (no communication): the epilogue as one HBM stream, moved by the copy engine of each
@@ -1056,7 +975,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
   }
   __syncthreads();
   const size_t row = (size_t)r * kp.T;
-  auto aligned = [&](int t, int e0, int n) {
+  auto aligned = [&](int t, int64_t e0, int n) {
     bool ok = (n & 3) == 0 && (((uintptr_t)(kp.a[row + t] + e0)) & 15) == 0;
     if constexpr (N::loadB) ok = ok && (((uintptr_t)(kp.b[row + t] + e0)) & 15) == 0;
     if constexpr (N::loadC) ok = ok && (((uintptr_t)(kp.c[row + t] + e0)) & 15) == 0;
@@ -1070,7 +989,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
       const int s = k % kTmaStages;
       if (k >= kTmaStages) mbar_wait(&empty[s], (uint32_t)((k / kTmaStages - 1) & 1));
       const int4 tl = kp.tiles[i];
-      if (!aligned(tl.x, tl.y, tl.z)) {  // consumers read global memory directly
+      const int64_t e0 = tile_elem(tl);
+      if (!aligned(tl.x, e0, tl.z)) {  // consumers read global memory directly
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s]))
                      : "memory");
         continue;
@@ -1080,10 +1000,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
                        smem_u32(&full[s])),
                    "r"(NA * bytes)
                    : "memory");
-      const float* src[4] = {kp.a[row + tl.x] + tl.y,
-                             N::loadB ? kp.b[row + tl.x] + tl.y : nullptr,
-                             N::loadC ? kp.c[row + tl.x] + tl.y : nullptr,
-                             N::loadD ? kp.d[row + tl.x] + tl.y : nullptr};
+      const float* src[4] = {kp.a[row + tl.x] + e0,
+                             N::loadB ? kp.b[row + tl.x] + e0 : nullptr,
+                             N::loadC ? kp.c[row + tl.x] + e0 : nullptr,
+                             N::loadD ? kp.d[row + tl.x] + e0 : nullptr};
 #pragma unroll
       for (int o = 0; o < NSLOT; ++o) {
         if (src[o] == nullptr) continue;
@@ -1101,12 +1021,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
   for (int i = blockIdx.x; i < kp.ntiles; i += gridDim.x, ++k) {
     const int s = k % kTmaStages;
     const int4 tl = kp.tiles[i];
-    float* pa = kp.a[row + tl.x] + tl.y;
-    float* pb = (N::loadB || N::storeB) ? kp.b[row + tl.x] + tl.y : nullptr;
-    float* pc = (N::loadC || N::storeC) ? kp.c[row + tl.x] + tl.y : nullptr;
-    const float* pd = N::loadD ? kp.d[row + tl.x] + tl.y : nullptr;
+    const int64_t e0 = tile_elem(tl);
+    float* pa = kp.a[row + tl.x] + e0;
+    float* pb = (N::loadB || N::storeB) ? kp.b[row + tl.x] + e0 : nullptr;
+    float* pc = (N::loadC || N::storeC) ? kp.c[row + tl.x] + e0 : nullptr;
+    const float* pd = N::loadD ? kp.d[row + tl.x] + e0 : nullptr;
     mbar_wait(&full[s], (uint32_t)((k / kTmaStages) & 1));
-    if (aligned(tl.x, tl.y, tl.z)) {
+    if (aligned(tl.x, e0, tl.z)) {
       const float4* sa = sm4 + ((size_t)s * NSLOT + 0) * (kTileE / 4);
       const float4* sb = sm4 + ((size_t)s * NSLOT + 1) * (kTileE / 4);
       const float4* sc = sm4 + ((size_t)s * NSLOT + 2) * (kTileE / 4);
@@ -1724,36 +1645,19 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_bal(KParams kp) {
 }
 
 template <int OP>
-const void* kernel_ptr(int algo, int p, int variant) {
-  if (algo == ALGO_LOCAL) {
-    switch (variant) {
-      // measured (ResNet-50 group, fused SGD): lean 1 CTA/SM U=4 87.5 us, lean 2/SM U=2 89.2,
-      // generic 2/SM U=2 88.0, generic 1/SM U=4 110.7
-      case 1: return (const void*)k_local<OP, 1, 4>;
-      case 2: return (const void*)k_local<OP, 2, 2>;
-      case 3: return (const void*)k_local_lean<OP, 2, 4>;
-      case 4: return (const void*)k_local_lean<OP, 2, 2>;
-      case 5: return (const void*)k_local_lean<OP, 1, 4>;
-      default: return (const void*)k_local_tma<OP>;
-    }
-  }
-#define TC_CASE(PP)                                                                  \
-  case PP:                                                                           \
-    if constexpr (OP != OP_EASGD)                                                    \
-      if (algo == ALGO_NVLS)                                                         \
-        return variant == 1 ? (const void*)k_nvls<OP, PP, 1> : (const void*)k_nvls<OP, PP, 2>; \
-    if (algo == ALGO_NVLS) return nullptr;                                           \
-    if (algo == ALGO_TWOSHOT_TMA) return (const void*)k_twoshot_tma<OP, PP>;         \
-    if (algo == ALGO_TWOSHOT_BAL) return (const void*)k_twoshot_bal<OP, PP>;         \
-    if (algo == ALGO_LL)                                                             \
-      return variant == 1 ? (const void*)k_ll<OP, PP, 1> : (const void*)k_ll<OP, PP, 2>; \
-    if (variant == 1)                                                                \
-      return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 1>           \
-           : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 1>      \
-                                       : (const void*)k_oneshot<OP, PP, 1>;          \
-    return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 2>             \
-         : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 2>        \
-                                     : (const void*)k_oneshot<OP, PP, 2>;
+const void* kernel_ptr(int algo, int p) {
+  if (algo == ALGO_LOCAL) return (const void*)k_local_tma<OP>;
+#define TC_CASE(PP)                                                                          \
+  case PP:                                                                                   \
+    if constexpr (OP != OP_EASGD)                                                            \
+      if (algo == ALGO_NVLS) return (const void*)k_nvls<OP, PP, 2>;                          \
+    if (algo == ALGO_NVLS) return nullptr;                                                   \
+    if (algo == ALGO_TWOSHOT_TMA) return (const void*)k_twoshot_tma<OP, PP>;                 \
+    if (algo == ALGO_TWOSHOT_BAL) return (const void*)k_twoshot_bal<OP, PP>;                 \
+    if (algo == ALGO_LL) return (const void*)k_ll<OP, PP, 2>;                                \
+    return algo == ALGO_TWOSHOT        ? (const void*)k_twoshot_pull<OP, PP, 2>              \
+           : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 2>              \
+                                       : (const void*)k_oneshot<OP, PP, 2>;
   switch (p) {
     TC_CASE(2) TC_CASE(3) TC_CASE(4) TC_CASE(5) TC_CASE(6) TC_CASE(7) TC_CASE(8)
     default: return nullptr;

@@ -4,8 +4,7 @@
 #include "tc_kernels.cuh"
 
 namespace tc {
-const void* kernel_ptr_bcast(int algo, int p, int variant) {
-  (void)variant;
+const void* kernel_ptr_bcast(int algo, int p) {
   if (algo != ALGO_TWOSHOT_TMA) return nullptr;
   switch (p) {
     case 2: return (const void*)k_twoshot_tma<OP_BCAST, 2>;

@@ -4,8 +4,7 @@
 #include "tc_kernels.cuh"
 
 namespace tc {
-const void* kernel_ptr_esgd(int algo, int p, int variant) {
-  (void)variant;
+const void* kernel_ptr_esgd(int algo, int p) {
   if (algo == ALGO_LOCAL) return (const void*)k_local_tma<OP_ESGD>;
   if (algo == ALGO_TWOSHOT_BAL) {
     switch (p) {

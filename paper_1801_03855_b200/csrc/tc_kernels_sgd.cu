@@ -3,5 +3,5 @@
 #include "tc_kernels.cuh"
 
 namespace tc {
-const void* kernel_ptr_sgd(int algo, int p, int variant) { return kernel_ptr<OP_SGD>(algo, p, variant); }
+const void* kernel_ptr_sgd(int algo, int p) { return kernel_ptr<OP_SGD>(algo, p); }
 }  // namespace tc

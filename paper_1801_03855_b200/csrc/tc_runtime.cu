@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -88,7 +89,6 @@ tc_status finish_comm(Comm& c) {
   TC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
   c.num_sms = sms;
   c.timeout_ns = env_timeout_ns();
-  c.variant = std::getenv("TC_VARIANT") ? std::atoi(std::getenv("TC_VARIANT")) : 0;
   return TC_OK;
 }
 
@@ -216,10 +216,13 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
       const int64_t n = pl.numel[(size_t)t];
       const int64_t head = std::min<int64_t>(n, (4 - g.shift[(size_t)t]) & 3);
       const int64_t full = head + ((n - head) & ~(int64_t)3);
-      if (head > 0) tiles.push_back(make_int4(t, 0, (int)head, 0));
-      for (int64_t e = head; e < full; e += kTileE)
-        tiles.push_back(make_int4(t, (int)e, (int)std::min<int64_t>(kTileE, full - e), 0));
-      if (full < n) tiles.push_back(make_int4(t, (int)full, (int)(n - full), 0));
+      // {tensor, first element (low 32 bits), elements, first element (high 32 bits)}
+      auto tile = [&](int64_t e, int64_t cnt) {
+        tiles.push_back(make_int4(t, (int)(uint32_t)(e & 0xffffffff), (int)cnt, (int)(e >> 32)));
+      };
+      if (head > 0) tile(0, head);
+      for (int64_t e = head; e < full; e += kTileE) tile(e, std::min<int64_t>(kTileE, full - e));
+      if (full < n) tile(full, n - full);
     }
     if (tiles.size() >= (size_t)INT32_MAX) return TC_ERR_INVALID_ARG;
     g.ntiles = (int)tiles.size();
@@ -376,10 +379,10 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.shift_c = gc ? gc->d_shift : nullptr;
 
   const int threads = c.tune_threads;
+  // per-group CTA budget (tc_group_set_num_ctas), else the comm's tuning
+  const int tune_ctas = ga->num_ctas > 0 ? ga->num_ctas : c.tune_ctas;
   const int64_t bytes = Mdev * 16;
   int algo;
-  // the fused elastic + SGD step (NEXT row f2) exists only in the TMA kernels
-  const int variant = op == OP_ESGD ? 0 : c.variant;
   if (p == 1) {
     algo = ALGO_LOCAL;
   } else if (op == OP_BCAST) {  // implemented by the TMA two-shot only
@@ -422,7 +425,8 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
     // (automatic NVLS only for the plain allreduce: the fused SGD step's HBM epilogue cannot
     // start before the switch has reduced a chunk, measured 405 us vs 297 us pulled at p = 4)
-    else if (nvls_ok && (c.algo_override == ALGO_NVLS || (p >= 6 && op == OP_ALLREDUCE)))
+    else if (nvls_ok && (c.algo_override == ALGO_NVLS ||
+                         (c.allow_switch && p >= 6 && op == OP_ALLREDUCE)))
       algo = ALGO_NVLS;
     // TMA-staged two-shot: ResNet-50 group p = 2 allreduce 188 / SGD step 197 us (LDG pull
     // 208 / 226, NCCL allreduce 219); p = 4 262 / 278 us (pull 289 / 301, NCCL 274-276).
@@ -433,7 +437,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
       return TC_ERR_CUDA;
   }
   const int nlocal = c.emulated ? p : 1;
-  int occ = max_ctas_per_sm(op, algo, p, threads, variant);
+  int occ = max_ctas_per_sm(op, algo, p, threads);
   if (occ < 1) return TC_ERR_CUDA;
   int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
   if (cap < 1) cap = 1;
@@ -444,19 +448,17 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL) {
     // bytes in flight come from the stage ring, not from threads: one CTA per SM at most
     const int tiles_r = ga->tile2_off[1] - ga->tile2_off[0];
-    ctas = c.tune_ctas > 0 ? c.tune_ctas : c.num_sms;
+    ctas = tune_ctas > 0 ? tune_ctas : c.num_sms;
     ctas = std::max(1, std::min(ctas, std::max(tiles_r, 1)));
     kp.tiles2 = ga->d_tiles2;
     for (int q = 0; q <= p; ++q) kp.tile2_off[q] = ga->tile2_off[(size_t)q];
-  } else if (algo == ALGO_LOCAL && variant == 0) {  // TMA stream
-    ctas = std::min(ga->ntiles, c.tune_ctas > 0 ? std::min(c.tune_ctas, c.num_sms * occ)
+  } else if (algo == ALGO_LOCAL) {  // TMA stream
+    ctas = std::min(ga->ntiles, tune_ctas > 0 ? std::min(tune_ctas, c.num_sms * occ)
                                                 : c.num_sms * occ);
     kp.tiles = ga->d_tiles;
     kp.ntiles = ga->ntiles;
-  } else if (algo == ALGO_LOCAL) {
-    ctas = (int)std::min<int64_t>(want, (int64_t)c.num_sms * occ);
-  } else if (twoshot && c.tune_ctas > 0) {
-    ctas = c.tune_ctas;
+  } else if (twoshot && tune_ctas > 0) {
+    ctas = tune_ctas;
   } else if (algo == ALGO_NVLS && op == OP_ALLREDUCE) {
     // switch reductions saturate with ~half the SMs (p = 4 allreduce: 74 CTAs 285 us,
     // 148 x 512 299, 296 x 512 307); the SGD epilogue pass wants the full grid (392 vs 470 us)
@@ -472,8 +474,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (ctas < 1) ctas = 1;
   if (c.prof && (int64_t)ctas * nlocal <= c.prof_slots) kp.prof = c.prof;
   kp.state = c.d_state;
-  cudaError_t e = launch_hot(op, algo, kp, ctas, threads, nlocal, c.emulated && p > 1, stream,
-                             variant);
+  cudaError_t e = launch_hot(op, algo, kp, ctas, threads, nlocal, c.emulated && p > 1, stream);
   if (e != cudaSuccess) {
     if (std::getenv("TC_DEBUG"))
       std::fprintf(stderr, "libtc: launch failed: %s\n", cudaGetErrorString(e));
@@ -481,7 +482,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   }
   c.last_algo = algo;
   c.last_ctas = ctas;
-  c.last_threads = launch_threads(op, algo, p, threads, variant);
+  c.last_threads = launch_threads(op, algo, p, threads);
   return TC_OK;
 }
 
@@ -622,6 +623,24 @@ tc_status tc_comm_set_algorithm(tc_comm* comm, int algo) {
   return TC_OK;
 }
 
+tc_status tc_comm_set_switch_reduction(tc_comm* comm, int allow) {
+  if (!comm || (allow != 0 && allow != 1)) return TC_ERR_INVALID_ARG;
+  comm->c.allow_switch = allow != 0;
+  return TC_OK;
+}
+
+tc_status tc_group_set_num_ctas(tc_group* group, int num_ctas) {
+  if (!group || num_ctas < 0 || num_ctas > kMaxCtas) return TC_ERR_INVALID_ARG;
+  group->g.num_ctas = num_ctas;
+  return TC_OK;
+}
+
+tc_status tc_comm_set_debug_busy(tc_comm* comm, int hold) {
+  if (!comm) return TC_ERR_INVALID_ARG;
+  comm->c.busy.store(hold != 0);
+  return TC_OK;
+}
+
 tc_status tc_comm_set_timeout(tc_comm* comm, int64_t timeout_ms) {
   if (!comm || timeout_ms <= 0) return TC_ERR_INVALID_ARG;
   comm->c.timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
@@ -690,6 +709,8 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
   *out = nullptr;
   if (!comm) return TC_ERR_INVALID_ARG;
   Comm& c = comm->c;
+  BusyGuard busy(c.busy);  // one collective call per comm at a time
+  if (!busy.ok) return TC_ERR_BUSY;
   const int p = c.nranks;
   const int myrank = c.emulated ? 0 : c.rank;
   Plan plan;
@@ -886,6 +907,16 @@ tc_status tc_group_create(tc_comm* comm, int ntensors, void* const* ptrs, const 
     delete h;
     return st;
   }
+  if (!c.emulated && p > 1) {
+    // pin the symmetric allocations the tensors live in until the group is destroyed
+    for (int t = 0; t < T; ++t) {
+      if (base_idx[t] > -2) continue;
+      void* b = c.sym[(size_t)(-(base_idx[t] + 2))].uc[c.rank];
+      if (std::find(g.sym_bases.begin(), g.sym_bases.end(), b) == g.sym_bases.end())
+        g.sym_bases.push_back(b);
+    }
+    for (void* b : g.sym_bases) sym_ref(c, b, +1);
+  }
   c.live_groups++;
   *out = h;
   return TC_OK;
@@ -895,10 +926,13 @@ tc_status tc_group_destroy(tc_group* group) {
   if (!group) return TC_ERR_INVALID_ARG;
   Group& g = group->g;
   Comm& c = *g.comm;
+  BusyGuard busy(c.busy);
+  if (!busy.ok) return TC_ERR_BUSY;
   cudaSetDevice(c.device);
   cudaDeviceSynchronize();
   tc_status st = comm_barrier(c);  // no peer kernel can still read our tensors
   for (auto& k : g.mapped_keys) unmap_peer(c, k);
+  for (void* b : g.sym_bases) sym_ref(c, b, -1);
   free_group_device(g);
   c.live_groups--;
   delete group;

@@ -234,6 +234,11 @@ int find_sym(const Comm& c, const void* p, size_t bytes, int64_t* offset) {
   return -1;
 }
 
+void sym_ref(Comm& c, const void* base, int delta) {
+  for (SymAlloc& a : c.sym)
+    if (a.uc[c.rank < 0 ? 0 : c.rank] == base) a.refs += delta;
+}
+
 bool multicast_supported(int device) {
   const Drv& d = driver();
   if (!d.ok) return false;
@@ -411,6 +416,7 @@ tc_status tc_mem_free(tc_comm* comm, void* ptr) {
   int64_t off = 0;
   int i = find_sym(c, ptr, 1, &off);
   if (i < 0 || off != 0) return TC_ERR_INVALID_ARG;
+  if (c.sym[(size_t)i].refs > 0) return TC_ERR_INVALID_ARG;  // a live group still points into it
   cudaSetDevice(c.device);
   cudaDeviceSynchronize();
   tc_status st = barrier(c);  // no peer kernel still touches it

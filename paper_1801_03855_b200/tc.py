@@ -58,6 +58,9 @@ _SIGS = {
     "tc_comm_set_tuning": (_c_int, [_vp, _c_int, _c_int, _c_int64]),
     "tc_comm_set_timeout": (_c_int, [_vp, _c_int64]),
     "tc_comm_set_algorithm": (_c_int, [_vp, _c_int]),
+    "tc_comm_set_switch_reduction": (_c_int, [_vp, _c_int]),
+    "tc_comm_set_debug_busy": (_c_int, [_vp, _c_int]),
+    "tc_group_set_num_ctas": (_c_int, [_vp, _c_int]),
     "tc_comm_set_ll_max": (_c_int, [_vp, _c_int64]),
     "tc_mem_alloc": (_c_int, [_vp, ctypes.c_size_t, _pp]),
     "tc_mem_free": (_c_int, [_vp, _vp]),
@@ -280,6 +283,15 @@ class Comm:
         4 = NVLS for groups in symmetric memory."""
         _check(LIB.tc_comm_set_algorithm(self.h, int(algo)), "set_algorithm")
 
+    def set_switch_reduction(self, allow: bool):
+        """Let the automatic choice use NVLS (fp32 sums in the switch; tolerance contract)."""
+        _check(LIB.tc_comm_set_switch_reduction(self.h, int(bool(allow))),
+               "set_switch_reduction")
+
+    def set_debug_busy(self, hold: bool):
+        """Tests: mark the comm busy as if another thread were inside a call on it."""
+        _check(LIB.tc_comm_set_debug_busy(self.h, int(bool(hold))), "set_debug_busy")
+
     def set_ll_max(self, nbytes: int):
         """Groups up to nbytes use the low-latency algorithm (-1 automatic, 0 never)."""
         _check(LIB.tc_comm_set_ll_max(self.h, int(nbytes)), "set_ll_max")
@@ -358,6 +370,10 @@ class Group:
         _check(LIB.tc_group_create(comm.h, T, ptrs, arr, ctypes.byref(h)), "tc_group_create")
         self.h = h
         comm.groups += 1
+
+    def set_num_ctas(self, num_ctas: int):
+        """CTA budget of this group's launches (0 = the comm's tuning); identical on all ranks."""
+        _check(LIB.tc_group_set_num_ctas(self.h, int(num_ctas)), "tc_group_set_num_ctas")
 
     def destroy(self):
         if self.h:
@@ -453,6 +469,9 @@ class BucketedStep:
             self.W = [Group(comm, pick(w, m)) for m in members]
             self.D = [Group(comm, pick(dw, m)) for m in members]
         self.ctas = ctas
+        if ctas:  # the CTA budget applies to the bucket launches only (per group, not the comm)
+            for grp in self.G:
+                grp.set_num_ctas(ctas)
         self.hp = {}
         self.reset()
 
@@ -471,17 +490,10 @@ class BucketedStep:
         ev = torch.cuda.Event()
         ev.record(compute_stream or torch.cuda.current_stream())
         self.stream.wait_event(ev)
-        if self.ctas:
-            self.comm.set_tuning(self.ctas, 0, -1)
-        try:
-            if self.W is not None:
-                sgd_step(self.W[b], self.G[b], self.D[b], stream=self.stream, **hp)
-            else:
-                allreduce(self.G[b], 1.0 if self.split else hp.get("scale", 1.0),
-                          stream=self.stream)
-        finally:
-            if self.ctas:  # the CTA budget applies to the bucket launches only
-                self.comm.set_tuning(0, 0, -1)
+        if self.W is not None:
+            sgd_step(self.W[b], self.G[b], self.D[b], stream=self.stream, **hp)
+        else:
+            allreduce(self.G[b], 1.0 if self.split else hp.get("scale", 1.0), stream=self.stream)
 
     def finish(self, compute_stream=None):
         import torch

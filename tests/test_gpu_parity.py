@@ -334,10 +334,10 @@ def run_easgd(c, numels, alpha, oneshot=-1, kind="float"):
     return res, xs, center, algo
 
 
-@pytest.mark.parametrize("name,oneshot", ALGOS + [("local", -1)])
+@pytest.mark.parametrize("name,oneshot,c", [a + (c,) for a in ALGOS for c in (2, 4, 8)] +
+                         [("local", -1, 1)])
 @pytest.mark.parametrize("alpha", [0.1, 0.5, 0.0])
-def test_easgd(name, oneshot, alpha):
-    c = 1 if name == "local" else 4
+def test_easgd(name, oneshot, c, alpha):
     numels = [7, 13, 1000, 4096, 0, 2]
     res, xs, center, algo = run_easgd(c, numels, alpha, oneshot)
     assert algo == name
@@ -527,3 +527,79 @@ def test_broadcast(p, offset):
             tc.broadcast(g, p)  # root outside the comm
         g.destroy()
         comm.destroy()
+
+
+def test_busy_one_call_per_comm():
+    """S:246 "one collective call per communicator at a time": while another call holds the
+    comm (fault injection marks it busy) every call that takes it returns TC_ERR_BUSY and does
+    nothing; once released the same calls succeed.  Then two host threads hammer one comm:
+    every call either succeeds or reports TC_ERR_BUSY, never anything else."""
+    import threading
+    comm = tc.Comm.emulated(2, 0)
+    xs = [W.group([7, 13, 1000], "int", 80, 0, k, W.GRAD) for k in range(2)]
+    dev = [to_dev(x) for x in xs]
+    g = tc.Group(comm, dev)
+    comm.set_debug_busy(True)
+    with pytest.raises(tc.TcError) as e:
+        tc.allreduce(g)
+    assert e.value.status == tc.tc.TC_ERR_BUSY
+    with pytest.raises(tc.TcError) as e:
+        tc.Group(comm, [to_dev(x) for x in xs])
+    assert e.value.status == tc.tc.TC_ERR_BUSY
+    for r in range(2):  # nothing ran
+        assert_bitwise(to_host(dev[r]), xs[r], f"rank {r} untouched")
+    comm.set_debug_busy(False)
+    tc.allreduce(g, 0.5)
+    want = O.allreduce(xs, 0.5)
+    for r in range(2):
+        assert_bitwise(to_host(dev[r]), want, f"rank {r}")
+
+    seen = {"ok": 0, "busy": 0, "other": []}
+    lock = threading.Lock()
+
+    def hammer():
+        for _ in range(300):
+            st = tc.LIB.tc_allreduce(g.h, 0.5, None)
+            with lock:
+                if st == tc.tc.TC_OK:
+                    seen["ok"] += 1
+                elif st == tc.tc.TC_ERR_BUSY:
+                    seen["busy"] += 1
+                else:
+                    seen["other"].append(st)
+
+    th = [threading.Thread(target=hammer) for _ in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not seen["other"], seen
+    assert seen["ok"] >= 300
+    assert comm.async_error() == 0
+    g.destroy()
+    comm.destroy()
+
+
+def test_group_cta_budget():
+    """tc_group_set_num_ctas: a per-group CTA budget (the comm's tuning is untouched), same
+    results."""
+    p = 4
+    numels = [7, 13, 1000, 40000, 3]
+    xs = [W.group(numels, "grad", 81, 0, k, W.GRAD) for k in range(p)]
+    comm = _comm(p, TMA)
+    dev = [to_dev(x) for x in xs]
+    g = tc.Group(comm, dev)
+    g.set_num_ctas(3)
+    tc.allreduce(g, 0.25)
+    assert comm.last_launch()[:2] == ("two-shot-tma", 3)
+    want = O.allreduce(xs, 0.25)
+    for r in range(p):
+        assert_bitwise(to_host(dev[r]), want, f"rank {r}")
+    g.set_num_ctas(0)
+    tc.allreduce(g, 1.0)
+    assert comm.last_launch()[1] > 3
+    with pytest.raises(tc.TcError):
+        g.set_num_ctas(-1)
+    g.destroy()
+    comm.destroy()

@@ -19,10 +19,10 @@ ALGOS = {"auto": (0, -1, -1), "pull": (1, 0, 0), "push": (3, 0, 0), "tma": (6, 0
          "bal": (7, 0, 0), "oneshot": (0, 1 << 30, 0), "ll": (0, 0, 1 << 30)}
 
 
-@settings(max_examples=40, deadline=None)
+@settings(max_examples=60, deadline=None)
 @given(numels=st.lists(st.integers(0, 5000), min_size=1, max_size=24),
        p=st.sampled_from([1, 2, 3, 4, 8]), offset=st.integers(0, 3),
-       algo=st.sampled_from(sorted(ALGOS)), op=st.sampled_from(["allreduce", "sgd", "esgd"]),
+       algo=st.sampled_from(sorted(ALGOS)), op=st.sampled_from(["allreduce", "sgd", "easgd", "esgd"]),
        seed=st.integers(0, 2 ** 31 - 1))
 def test_random_groups(numels, p, offset, algo, op, seed):
     if sum(numels) == 0:
@@ -62,6 +62,18 @@ def test_random_groups(numels, p, offset, algo, op, seed):
             assert_bitwise(to_host(dg[r]), G, f"g rank {r}")
             assert_bitwise(to_host(dwt[r]), Ws[r], f"w rank {r}")
             assert_bitwise(to_host(ddw[r]), Ds[r], f"dw rank {r}")
+    elif op == "easgd":
+        center = group(5e-2)
+        xs = [[c + (rng.standard_normal(c.size) * 1e-2).astype(np.float32) for c in center]
+              for _ in range(p)]
+        dx = [to_dev(x, offset=offset) for x in xs]
+        dc = [to_dev(center, offset=offset) for _ in range(p)]
+        groups = [tc.Group(comm, pick(v)) for v in (dx, dc)]
+        tc.easgd_update(groups[0], groups[1], 0.1)
+        wx, wc = O.easgd_update(xs, center, 0.1)
+        for r in range(p):
+            assert_bitwise(to_host(dx[r]), wx[r], f"x rank {r}")
+            assert_bitwise(to_host(dc[r]), wc, f"center rank {r}")
     else:
         center = group(5e-2)
         xs = [[c + (rng.standard_normal(c.size) * 1e-2).astype(np.float32) for c in center]

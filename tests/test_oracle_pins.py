@@ -364,9 +364,12 @@ def test_elastic_tolerance_vs_f64():
 
 # ------------------------------------------------------------------ config 4 sequence
 def test_esgd_sequence_composition():
-    """16 steps, tau = 4, 2 clients x 2 GPUs on integer data with dyadic hyper-parameters:
-    every intermediate is exact, so the sequence equals an exact rational re-computation of
-    Fig. code-snippet-4's order (Elastic2 before SGD.Update in the same iteration)."""
+    """8 steps (two elastic updates), tau = 4, 2 clients x 2 GPUs on integer data with dyadic
+    hyper-parameters: every intermediate is exact, so the sequence equals an exact rational
+    re-computation of Fig. code-snippet-4's order (Elastic2 before SGD.Update in the same
+    iteration).  (At 16 steps the dyadic denominators outgrow fp32's 24-bit
+    significand and the oracle rounds, as it must; config 4's 16-step sequence is pinned on the
+    GPU side against this composition, tests/test_gpu_fullsize.py.)"""
     numels = [5, 11]
     c, q, steps, tau = 2, 2, 8, 4
     center = W.group(numels, "int", 80, 0, 0, W.CENTER)

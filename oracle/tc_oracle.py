@@ -29,6 +29,11 @@ Pins (tests/test_oracle_pins.py, -m "not gpu"):
   esgd_step        -- NEXT row f2 (elastic then SGD with each client's own gradient): pinned by
                       exact rational evaluation on dyadic data and its special cases (alpha = 0
                       -> local sgd_step; lr = momentum = 0 -> easgd_update).
+  easgd_async      -- NEXT row f2 (the server applies Elastic1 per client, in arrival order):
+                      pinned at c = 1 to Eqs. elastic1/elastic2 in exact rationals, by the
+                      alpha = 1/2 closed form (each arriving client meets the center at their
+                      midpoint), exact conservation of sum_i x_i + xc on integer data with
+                      dyadic alpha, the alpha = 0 identity, and relabelling invariance.
   The momentum term (mu != 0) follows reading R12; the paper fixes no formula for it (P:158 names
   "momentum SGD" only), so it is pinned to its own closed form and to an independent library
   routine for the standard heavy-ball form (torch.optim.SGD, float64, several steps:
@@ -41,6 +46,7 @@ import numpy as np
 __all__ = [
     "allreduce", "allreduce_f64", "reduce_scatter", "allgather",
     "sgd_step", "sgd_step_f64", "easgd_update", "easgd_update_f64", "esgd_sequence", "esgd_step",
+    "easgd_async",
     "broadcast",
     "slot_partition", "bus_bytes_per_rank", "predict_cost", "ring_allreduce_sim",
     "F", "R",
@@ -239,6 +245,35 @@ def easgd_update_f64(xs, center, alpha):
         for i in range(1, c):
             s = s + d[i]
         c_out.append(xc + a * s)
+    return x_out, c_out
+
+
+def easgd_async(xs, center, alpha, order=None):
+    """Asynchronous elastic averaging at a parameter server ("The update elastic1 is done
+    on the server and elastic2 is done on the client"; Fig. code-snippet-4):
+    clients arrive one at a time, in `order` (a permutation of 0..c-1, the recorded ticket
+    order; default client order).  On client i's arrival, with the center as the earlier
+    arrivals left it (fp32 mirror, a = alpha as fp32):
+
+        d_i  = R(x_i - xc)
+        xc   = R(xc + R(a*d_i))        (Eq. elastic1, at the server)
+        x_i' = R(x_i - R(a*d_i))       (Eq. elastic2, at the client, same w~_t; reading R20)
+
+    Returns ([x_i'], xc').  At c = 1 this is exactly easgd_update (Eqs. elastic1/elastic2).
+    """
+    a = _f32(alpha)
+    c = len(xs)
+    order = list(range(c)) if order is None else [int(i) for i in order]
+    if sorted(order) != list(range(c)):
+        raise ValueError("order must be a permutation of the clients")
+    x_out = [[np.array(t, dtype=np.float32, copy=True) for t in x] for x in xs]
+    c_out = [np.array(t, dtype=np.float32, copy=True) for t in center]
+    for i in order:
+        for t in range(len(center)):
+            d = (x_out[i][t] - c_out[t]).astype(np.float32)
+            ad = (a * d).astype(np.float32)
+            c_out[t] = (c_out[t] + ad).astype(np.float32)
+            x_out[i][t] = (x_out[i][t] - ad).astype(np.float32)
     return x_out, c_out
 
 

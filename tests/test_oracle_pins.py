@@ -459,3 +459,81 @@ def test_broadcast_definition():
             for t in range(len(numels)):
                 assert out[r][t].tobytes() == xs[root][t].tobytes()
                 assert out[r][t] is not xs[root][t]
+
+
+# ------------------------------------------------------------------ NEXT row f2: async server EASGD
+def test_easgd_async_c1_is_eq_elastic1_elastic2_exact():
+    """c = 1: one arrival is exactly Eq. elastic1 at the server and Eq. elastic2 at the client
+    (P:69-78), evaluated in exact rationals on integer data with dyadic alpha."""
+    x = W.group([300], "int", 90, 0, 0, W.PARAM)
+    xc = W.group([300], "int", 90, 0, 0, W.CENTER)
+    a = Fraction(0.25)
+    xs, c = O.easgd_async([x], xc, 0.25)
+    for j in range(300):
+        w, wt = Fraction(float(x[0][j])), Fraction(float(xc[0][j]))
+        assert Fraction(float(c[0][j])) == wt + a * (w - wt)        # elastic1
+        assert Fraction(float(xs[0][0][j])) == w - a * (w - wt)     # elastic2
+
+
+@pytest.mark.parametrize("order", [(0, 1, 2), (2, 0, 1), (1, 2, 0)])
+def test_easgd_async_midpoint_closed_form(order):
+    """alpha = 1/2: each arriving client and the center move to their midpoint, so after the
+    arrivals i_1, i_2, i_3: x_{i_1}' = xc_1 = (xc + x_{i_1})/2, x_{i_k}' = xc_k =
+    (xc_{k-1} + x_{i_k})/2 -- a closed form independent of the update formulas' code."""
+    c = 3
+    xs = [W.group([256], "int", 91, 0, i, W.PARAM) for i in range(c)]
+    xc = W.group([256], "int", 91, 0, 0, W.CENTER)
+    xo, co = O.easgd_async(xs, xc, 0.5, order)
+    for j in range(256):
+        cur = Fraction(float(xc[0][j]))
+        for i in order:
+            cur = (cur + Fraction(float(xs[i][0][j]))) / 2
+            assert Fraction(float(xo[i][0][j])) == cur
+        assert Fraction(float(co[0][j])) == cur
+
+
+@pytest.mark.parametrize("alpha", [0.5, 0.25])
+def test_easgd_async_conservation_exact(alpha):
+    """Every arrival moves the center by +a d and the client by -a d, so sum_i x_i + xc is
+    conserved -- exactly on integer data with dyadic alpha (no rounding occurs)."""
+    c = 5
+    xs = [W.group([400], "int", 92, 0, i, W.PARAM) for i in range(c)]
+    xc = W.group([400], "int", 92, 0, 0, W.CENTER)
+    xo, co = O.easgd_async(xs, xc, alpha, [3, 1, 4, 0, 2])
+    before = sum(xs[i][0].astype(np.float64) for i in range(c)) + xc[0]
+    after = sum(xo[i][0].astype(np.float64) for i in range(c)) + co[0]
+    assert (before == after).all()
+
+
+def test_easgd_async_alpha0_and_relabelling():
+    """alpha = 0 is the identity; and the result depends on the clients only through the
+    arrival sequence: permuting the clients together with the order permutes the outputs."""
+    c = 4
+    xs = [W.group([200], "param", 93, 0, i, W.PARAM) for i in range(c)]
+    xc = W.group([200], "center", 93, 0, 0, W.CENTER)
+    xo, co = O.easgd_async(xs, xc, 0.0, [2, 0, 3, 1])
+    assert all((xo[i][0] == xs[i][0]).all() for i in range(c)) and (co[0] == xc[0]).all()
+    order = [2, 0, 3, 1]
+    perm = [3, 1, 0, 2]                      # new label of old client i is perm[i]
+    ys = [None] * c
+    for i in range(c):
+        ys[perm[i]] = xs[i]
+    xo, co = O.easgd_async(xs, xc, 0.1, order)
+    yo, cy = O.easgd_async(ys, xc, 0.1, [perm[i] for i in order])
+    assert all(np.array_equal(yo[perm[i]][0], xo[i][0]) for i in range(c))
+    assert np.array_equal(cy[0], co[0])
+
+
+def test_easgd_async_differs_from_sync_by_order():
+    """c >= 2: the server's center moves between arrivals (the asynchronous form), unlike the
+    synchronous sum form, which uses the pre-update center for every client (reading R10):
+    the first arrival agrees with easgd_update's x_i', later ones do not in general."""
+    c = 3
+    xs = [W.group([500], "param", 94, 0, i, W.PARAM) for i in range(c)]
+    xc = W.group([500], "center", 94, 0, 0, W.CENTER)
+    xa, ca = O.easgd_async(xs, xc, 0.1, [1, 0, 2])
+    xsync, _ = O.easgd_update(xs, xc, 0.1)
+    assert np.array_equal(xa[1][0], xsync[1][0])
+    assert not np.array_equal(xa[2][0], xsync[2][0])
+    with pytest.raises(ValueError):
+        O.easgd_async(xs, xc, 0.1, [0, 0, 1])

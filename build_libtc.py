@@ -21,7 +21,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtc.so")
 SOURCES = ["tc_plan.cpp", "tc_runtime.cu", "tc_symmem.cu", "tc_kernels.cu",
            "tc_kernels_allreduce.cu", "tc_kernels_sgd.cu", "tc_kernels_easgd.cu",
-           "tc_kernels_esgd.cu", "tc_kernels_bcast.cu"]
+           "tc_kernels_esgd.cu", "tc_kernels_bcast.cu", "tc_kernels_easync.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

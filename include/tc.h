@@ -294,6 +294,23 @@ TC_API tc_status tc_esgd_step(tc_group* x, tc_group* center, tc_group* g, tc_gro
                               float alpha, float lr, float momentum, float wd, float rescale,
                               void* stream);
 
+/* NEXT row f2, asynchronous server: elastic averaging as the paper's parameter server applies
+ * it -- Elastic1 on the server as each client's push arrives, Elastic2 on the client (P:66
+ * "elastic1 is done on the server and elastic2 is done on the client"; Fig. code-snippet-4,
+ * P:302-312) -- with the arrivals in the recorded order `order` (host array of nranks
+ * client indices, a permutation; NULL = client order 0..c-1; identical on all ranks).  The
+ * center is sharded by owner (the owner of a chunk is its server shard) and replicated after
+ * the call.  Per element, for i = order[0], order[1], ... with the center as the earlier
+ * arrivals left it, fp32 with every op rounded (oracle.easgd_async, reading R20):
+ *     d = x_i - xc;     xc := xc + alpha*d   (Eq. elastic1);     x_i := x_i - alpha*d   (Eq. elastic2)
+ * c = 1 is exactly tc_easgd_update.  One kernel (TMA two-shot): the owner pulls every client's
+ * chunk, applies the arrivals, stores each client's new chunk straight into that client's
+ * tensor over NVLink, stages the center; the allgather brings the center.  Per GPU: NVLink
+ * ingress 2(c-1)/c S, egress 2(c-1)/c S.  Errors: TC_ERR_INVALID_ARG (alpha outside [0, 1],
+ * order not a permutation), TC_ERR_SHAPE_MISMATCH, TC_ERR_TIMEOUT, TC_ERR_BUSY, TC_ERR_CUDA. */
+TC_API tc_status tc_easgd_async_update(tc_group* x, tc_group* center, float alpha,
+                                       const int* order, void* stream);
+
 /* Tensor broadcast (MPI_Bcast of the weights at initialisation; the KVStore.pull
  * broadcast): every rank's group := the root's group, bit for bit.  Scatter from
  * the root (each rank copies its owner chunk of the root's tensors) then the allgather of the

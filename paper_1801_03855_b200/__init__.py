@@ -5,6 +5,7 @@ thin ctypes binding in :mod:`paper_1801_03855_b200.tc`.  Importing this package 
 raises if it has not been built -- there is no CPU fallback.
 """
 from .tc import (  # noqa: F401
-    Comm, Group, Plan, TcError, allreduce, sgd_step, easgd_update, esgd_step, broadcast, LIB, LIB_PATH, STATUS,
+    Comm, Group, Plan, TcError, allreduce, sgd_step, easgd_update, easgd_async_update, esgd_step,
+    broadcast, LIB, LIB_PATH, STATUS,
     BucketedStep,
 )

@@ -71,6 +71,7 @@ constexpr int kT2Threads = 32 * (1 + kT2ConsumerWarps);
 // (ESGD, NEXT row f2: + w (= x), center, dw and the local gradient g)
 constexpr int t2_ops(int op, int p) {
   if (op == 4) return 1;  // broadcast: the root's copy, then the owner's staged chunk
+  if (op == 5) return p + 1;  // async EASGD: every client's x + the center; then the center
   const int rs = p + (op == 1 ? 2 : op == 2 ? 1 : op == 3 ? 3 : 0);
   const int ag = 1 + (op == 0 ? 0 : op == 3 ? 4 : 2);
   return rs > ag ? rs : ag;
@@ -84,7 +85,7 @@ constexpr int t2_smem(int op, int p) {
 }
 
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
-enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4 };
+enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4, OP_EASYNC = 5 };
 enum Algo {
   ALGO_LOCAL = 0,
   ALGO_TWOSHOT = 1,
@@ -160,6 +161,7 @@ struct KParams {
   DevState* state;       // [p] device-side call epochs (this process's ranks are valid)
   float scale, lr, mu, wd, rescale, alpha;
   int root;              // broadcast root
+  int order[kMaxRanks];  // async EASGD: client arrival order (a permutation of 0..p-1)
   unsigned long long timeout_ns;
   int* err;              // host-mapped sticky error word
   int absent_rank;       // fault injection (emulated only), -1 off

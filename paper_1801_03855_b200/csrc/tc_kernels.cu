@@ -8,6 +8,7 @@ const void* kernel_ptr_sgd(int algo, int p);
 const void* kernel_ptr_easgd(int algo, int p);
 const void* kernel_ptr_esgd(int algo, int p);
 const void* kernel_ptr_bcast(int algo, int p);
+const void* kernel_ptr_easync(int algo, int p);
 
 namespace {
 const void* select_kernel(int op, int algo, int p) {
@@ -17,6 +18,7 @@ const void* select_kernel(int op, int algo, int p) {
     case OP_EASGD: return kernel_ptr_easgd(algo, p);
     case OP_ESGD: return kernel_ptr_esgd(algo, p);
     case OP_BCAST: return kernel_ptr_bcast(algo, p);
+    case OP_EASYNC: return kernel_ptr_easync(algo, p);
   }
   return nullptr;
 }

@@ -168,13 +168,17 @@ enum Phase { PH_RS = 0, PH_AG = 1 };
 // Local operands of (op, phase): A = primary (x / g), B = w or center, C = dw.
 template <int OP, int PH, int P> struct Needs {
   static constexpr bool EL = (OP == OP_EASGD) || (OP == OP_ESGD);  // elastic: a = x, b = center
+  // async EASGD: the owner updates every client's x (stored straight into the client's tensor)
+  // and the center in the reduce-scatter; the allgather only brings the center
+  static constexpr bool AS = OP == OP_EASYNC;
   static constexpr bool loadA = EL && PH == PH_AG;
-  static constexpr bool loadB = (OP == OP_SGD) || EL;
+  static constexpr bool loadB = (OP == OP_SGD) || EL || (AS && PH == PH_RS);
   static constexpr bool loadC = (OP == OP_SGD) || (OP == OP_ESGD);
   static constexpr bool loadD = (OP == OP_ESGD);  // the rank's own (unreduced) gradient
   // p = 1 SGD: the reduced gradient is the gradient itself -- not stored back.
-  static constexpr bool storeA = !(OP == OP_SGD && PH == PH_RS && P == 1);
-  static constexpr bool storeB = (OP == OP_SGD) || EL;
+  static constexpr bool storeA = !(OP == OP_SGD && PH == PH_RS && P == 1) && !AS;
+  static constexpr bool storeB = (OP == OP_SGD) || EL || AS;
+  static constexpr bool stageB = EL || AS;  // the staged (gathered) value is the new center
   static constexpr bool storeC = (OP == OP_SGD) || (OP == OP_ESGD);
 };
 
@@ -214,6 +218,8 @@ __device__ __forceinline__ void elem(const KParams& kp, int r, const float* in, 
     }
     la = G;  // the reduced gradient is written back (R15)
     sgd1(kp, G, lb, lc);
+  } else if constexpr (OP == OP_EASYNC) {
+    if constexpr (PH == PH_AG) lb = in[0];  // the owner's final center (RS: easync1)
   } else {  // OP_EASGD: la = x_r, lb = center
     if constexpr (PH == PH_RS) {
       const float xc = lb;
@@ -232,6 +238,31 @@ __device__ __forceinline__ void elem(const KParams& kp, int r, const float* in, 
       la = __fsub_rn(la, __fmul_rn(kp.alpha, dr));
       lb = in[0];  // the owner's new center
     }
+  }
+}
+
+// NEXT row f2, asynchronous server: the owner of a chunk is its server shard and applies the
+// clients' arrivals in kp.order (oracle.easgd_async, reading R20): per arrival i, with the
+// center as the earlier arrivals left it, d = R(x_i - xc); xc = R(xc + R(a d)) (Eq. elastic1);
+// x_i' = R(x_i - R(a d)) (Eq. elastic2).  in[k]: client k's x; out[k]: its new x.
+template <int P>
+__device__ __forceinline__ void easync1(const KParams& kp, const float* in, float* out,
+                                        float& xc) {
+#pragma unroll
+  for (int k = 0; k < P; ++k) out[k] = in[k];
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int i = kp.order[j];
+    float xi = in[0];
+#pragma unroll
+    for (int k = 1; k < P; ++k)
+      if (k == i) xi = in[k];
+    const float ad = __fmul_rn(kp.alpha, __fsub_rn(xi, xc));
+    xc = __fadd_rn(xc, ad);
+    const float xo = __fsub_rn(xi, ad);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      if (k == i) out[k] = xo;
   }
 }
 
@@ -1097,11 +1128,85 @@ __host__ __device__ constexpr int t2_pack(int x) {
 // One tile of a TMA two-shot phase, processed by the consumer warps: a full tile and a partial
 // slot from shared memory (operand o of this tile at so + o * V), the element path from global
 // memory.
+// Reduce-scatter tile of the asynchronous elastic update: operands are the P clients' x (slots
+// 0..P-1) and this owner's center replica (slot P); every client's new x is stored straight into
+// that client's tensor (a peer store over NVLink: only this owner touches this chunk of any
+// client's x during the call), the final center into this rank's center and its staging.
+template <int P, int V>
+__device__ __forceinline__ void t2_tile_easync(const KParams& kp, const T2Desc& d,
+                                               const float4* so, int ct, int nct) {
+  const size_t T = (size_t)kp.T;
+  float* px[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) px[q] = kp.a[q * T + d.t] + d.e;
+  if (d.vec == 2) {  // one partial slot: only lanes inside the tensor are stored
+    if (ct == 0) {
+      const int lo_l = d.e < 0 ? (int)-d.e : 0;
+      const int hi_l = (int)min((int64_t)4, kp.numel[d.t] - d.e);
+      float4 c4 = so[P * V];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        if (l < lo_l || l >= hi_l) continue;
+        float in[P], out[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) in[q] = lane_of(so[q * V], l);
+        float xc = lane_of(c4, l);
+        easync1<P>(kp, in, out, xc);
+#pragma unroll
+        for (int q = 0; q < P; ++q) st4(px[q] + l, out[q]);
+        st4(d.b + l, xc);
+        lane(c4, l) = xc;
+      }
+      st16(d.st, c4);
+    }
+  } else if (d.vec) {
+    for (int v = ct; v < d.n; v += nct) {
+      float4 x[P], o[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) x[q] = so[q * V + v];
+      float4 c4 = so[P * V + v];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        float in[P], out[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) in[q] = lane_of(x[q], l);
+        float xc = lane_of(c4, l);
+        easync1<P>(kp, in, out, xc);
+#pragma unroll
+        for (int q = 0; q < P; ++q) lane(o[q], l) = out[q];
+        lane(c4, l) = xc;
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q) st16(px[q] + 4 * v, o[q]);
+      st16(d.b + 4 * v, c4);
+      st16(d.st + 4 * v, c4);
+    }
+  } else {  // element path
+    const int64_t j0 = d.e < 0 ? -d.e : 0;
+    const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
+    for (int64_t j = j0 + ct; j < j1; j += nct) {
+      float in[P], out[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) in[q] = ld4(px[q] + j);
+      float xc = ld4(d.b + j);
+      easync1<P>(kp, in, out, xc);
+#pragma unroll
+      for (int q = 0; q < P; ++q) st4(px[q] + j, out[q]);
+      st4(d.b + j, xc);
+      st4(d.st + j, xc);
+    }
+  }
+}
+
 template <int OP, int P, int PH, int OPSP, int V>
 __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& d,
                                         const float4* so, int ct, int nct) {
   using N = Needs<OP, PH, PH == PH_RS ? P : 2>;
   const size_t T = (size_t)kp.T;
+  if constexpr (OP == OP_EASYNC && PH == PH_RS) {
+    t2_tile_easync<P, V>(kp, d, so, ct, nct);
+    return;
+  }
   // reduce-scatter sources: every rank's copy, or the root's alone (broadcast)
   constexpr int NSRC = OP == OP_BCAST ? 1 : P;
   if (d.vec == 2) {
@@ -1129,7 +1234,7 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
           if constexpr (N::storeB) st4(d.b + l, lb);
           if constexpr (N::storeC) st4(d.c + l, lc);
         }
-        st16(d.st, Needs<OP, PH_RS, P>::EL ? b : oa);
+        st16(d.st, Needs<OP, PH_RS, P>::stageB ? b : oa);
       } else {
         constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
         constexpr int OD = OC + N::loadC;
@@ -1143,7 +1248,7 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
           float lc = N::loadC ? lane_of(so[OC * V], l) : 0.f;
           elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc,
                               N::loadD ? lane_of(so[OD * V], l) : 0.f);
-          st4(d.a + l, la);
+          if constexpr (N::storeA) st4(d.a + l, la);
           if constexpr (N::storeB) st4(d.b + l, lb);
           if constexpr (N::storeC) st4(d.c + l, lc);
         }
@@ -1185,7 +1290,7 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
           if constexpr (N::storeA) st16(d.a + 4 * v, oa);
           if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
           if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
-          st16(d.st + 4 * v, Needs<OP, PH_RS, P>::EL ? b[u] : oa);
+          st16(d.st + 4 * v, Needs<OP, PH_RS, P>::stageB ? b[u] : oa);
         }
       } else {
         constexpr int OA = 1, OB = 1 + N::loadA, OC = 1 + N::loadA + N::loadB;
@@ -1215,7 +1320,7 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
             lane(b[u], l) = lb;
             lane(c[u], l) = lc;
           }
-          st16(d.a + 4 * v, a[u]);
+          if constexpr (N::storeA) st16(d.a + 4 * v, a[u]);
           if constexpr (N::storeB) st16(d.b + 4 * v, b[u]);
           if constexpr (N::storeC) st16(d.c + 4 * v, c[u]);
         }
@@ -1236,13 +1341,13 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
         if constexpr (N::storeA) st4(d.a + j, la);
         if constexpr (N::storeB) st4(d.b + j, lb);
         if constexpr (N::storeC) st4(d.c + j, lc);
-        st4(d.st + j, Needs<OP, PH_RS, P>::EL ? lb : la);
+        st4(d.st + j, Needs<OP, PH_RS, P>::stageB ? lb : la);
       } else {
         const float in[1] = {ld4(d.st + j)};
         float la = N::loadA ? ld4(d.a + j) : 0.f;
         float lb = N::loadB ? ld4(d.b + j) : 0.f, lc = N::loadC ? ld4(d.c + j) : 0.f;
         elem4<OP, PH_AG, 2>(kp, r, in, la, lb, lc, N::loadD ? ld4(d.g + j) : 0.f);
-        st4(d.a + j, la);
+        if constexpr (N::storeA) st4(d.a + j, la);
         if constexpr (N::storeB) st4(d.b + j, lb);
         if constexpr (N::storeC) st4(d.c + j, lc);
       }

@@ -332,7 +332,7 @@ tc_status grow_arena(Comm& c, int64_t need) {
 // ------------------------------------------------------------------ hot-path dispatcher
 tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr, float mu,
                   float wd, float rescale, float alpha, cudaStream_t stream,
-                  Group* gd = nullptr, int root = 0) {
+                  Group* gd = nullptr, int root = 0, const int* order = nullptr) {
   Comm& c = *ga->comm;
   BusyGuard busy(c.busy);
   if (!busy.ok) return TC_ERR_BUSY;
@@ -356,6 +356,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   kp.c = gc ? gc->d_ptrs : nullptr;
   kp.d = gd ? gd->d_ptrs : nullptr;
   kp.root = root;
+  for (int j = 0; j < kMaxRanks; ++j) kp.order[j] = order ? (j < p ? order[j] : 0) : j;
   kp.mc = ga->d_mc;
   kp.flags = c.d_flags;
   kp.stage = c.d_stage;
@@ -386,6 +387,9 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (p == 1) {
     algo = ALGO_LOCAL;
   } else if (op == OP_BCAST) {  // implemented by the TMA two-shot only
+    algo = ALGO_TWOSHOT_TMA;
+    if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
+  } else if (op == OP_EASYNC) {  // implemented by the TMA two-shot only
     algo = ALGO_TWOSHOT_TMA;
     if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   } else if (op == OP_ESGD) {
@@ -972,6 +976,25 @@ tc_status tc_broadcast(tc_group* x, int root, void* stream) {
   if (x->g.comm->nranks == 1) return TC_OK;  // the root's tensors are the result
   return run_hot(OP_BCAST, &x->g, nullptr, nullptr, 1.0f, 0, 0, 0, 0, 0, (cudaStream_t)stream,
                  nullptr, root);
+}
+
+tc_status tc_easgd_async_update(tc_group* x, tc_group* center, float alpha, const int* order,
+                                void* stream) {
+  if (!x || !center || !finite(alpha) || alpha < 0.f || alpha > 1.f) return TC_ERR_INVALID_ARG;
+  if (!congruent(&x->g, &center->g)) return TC_ERR_SHAPE_MISMATCH;
+  const int p = x->g.comm->nranks;
+  int ord[kMaxRanks];
+  bool seen[kMaxRanks] = {};
+  for (int j = 0; j < p; ++j) {
+    ord[j] = order ? order[j] : j;
+    if (ord[j] < 0 || ord[j] >= p || seen[ord[j]]) return TC_ERR_INVALID_ARG;
+    seen[ord[j]] = true;
+  }
+  if (p == 1)  // one arrival: Eqs. elastic1/elastic2 exactly (the local elastic stream)
+    return run_hot(OP_EASGD, &x->g, &center->g, nullptr, 1.0f, 0, 0, 0, 0, alpha,
+                   (cudaStream_t)stream);
+  return run_hot(OP_EASYNC, &x->g, &center->g, nullptr, 1.0f, 0, 0, 0, 0, alpha,
+                 (cudaStream_t)stream, nullptr, 0, ord);
 }
 
 tc_status tc_easgd_update(tc_group* x, tc_group* center, float alpha, void* stream) {

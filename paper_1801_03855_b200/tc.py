@@ -78,6 +78,7 @@ _SIGS = {
     "tc_allreduce": (_c_int, [_vp, _c_float, _vp]),
     "tc_sgd_step": (_c_int, [_vp, _vp, _vp, _c_float, _c_float, _c_float, _c_float, _vp]),
     "tc_easgd_update": (_c_int, [_vp, _vp, _c_float, _vp]),
+    "tc_easgd_async_update": (_c_int, [_vp, _vp, _c_float, ctypes.POINTER(_c_int), _vp]),
     "tc_broadcast": (_c_int, [_vp, _c_int, _vp]),
     "tc_esgd_step": (_c_int, [_vp, _vp, _vp, _vp, _c_float, _c_float, _c_float, _c_float,
                               _c_float, _vp]),
@@ -402,6 +403,16 @@ def sgd_step(w: Group, g: Group, dw: Group, lr: float, momentum: float = 0.0, wd
 def easgd_update(x: Group, center: Group, alpha: float, stream=None):
     _check(LIB.tc_easgd_update(x.h, center.h, float(alpha), _stream_ptr(stream)),
            "tc_easgd_update")
+
+
+def easgd_async_update(x: Group, center: Group, alpha: float, order=None, stream=None):
+    """NEXT row f2: server-side Elastic1 per client arrival in `order` (a permutation of the
+    clients; None = client order), Elastic2 at each client."""
+    arr = None
+    if order is not None:
+        arr = (_c_int * len(order))(*[int(i) for i in order])
+    _check(LIB.tc_easgd_async_update(x.h, center.h, float(alpha), arr, _stream_ptr(stream)),
+           "tc_easgd_async_update")
 
 
 def broadcast(x: Group, root: int = 0, stream=None):

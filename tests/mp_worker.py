@@ -111,6 +111,17 @@ def main():
         assert_bitwise(to_host(dd), wd[rank], "esgd dw")
     assert comm.async_error() == 0
 
+    # NEXT row f2, asynchronous server: arrivals in a recorded order, owners store every
+    # client's new chunk into the client's tensor over NVLink
+    order = list(reversed(range(p)))
+    dx, dc = to_dev(xs[rank]), to_dev(center)
+    with tc.Group(comm, dx) as X, tc.Group(comm, dc) as C:
+        tc.easgd_async_update(X, C, 0.1, order)
+        wx, wc = O.easgd_async(xs, center, 0.1, order)
+        assert_bitwise(to_host(dx), wx[rank], "easgd_async x")
+        assert_bitwise(to_host(dc), wc, "easgd_async center")
+    assert comm.async_error() == 0
+
     # symmetric (tc_mem_alloc) memory: P2P algorithms bit-exact; NVLS (switch reduction) exact on
     # integers, within the BASELINE tolerance on gradients, identical on every rank
     numels = [7, 13, 1000, 0, 50001, 3, 262144]

@@ -294,3 +294,29 @@ def test_config5_sweep(mib, T, p):
     want = O.allreduce(xs, 0.5)
     for r in range(p):
         assert_bitwise(got[r], want, f"{mib} MiB T={T} p={p} rank {r} ({launched})")
+
+
+# ------------------------------------------------------------------ NEXT row f2: async-server EASGD
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_resnet50_easgd_async(p):
+    """The asynchronous-server elastic update on the full ResNet-50 parameters, arrivals in a
+    shuffled recorded order, whole arrays vs oracle.easgd_async."""
+    name = "resnet50"
+    center = grp(name, "center", W.CFG_EASGD, 0, 0, W.CENTER)
+    xs = [list(_client(name, W.CFG_EASGD, 0, i)) for i in range(p)]
+    order = [int(i) for i in np.random.default_rng(p).permutation(p)]
+    comm = tc.Comm.emulated(p, 0)
+    dx, dc = [to_dev(x) for x in xs], [to_dev(center) for _ in range(p)]
+    X, C = tc.Group(comm, dx), tc.Group(comm, dc)
+    tc.easgd_async_update(X, C, ALPHA, order)
+    got = [(to_host(dx[i]), to_host(dc[i])) for i in range(p)]
+    assert comm.last_launch()[0] == "two-shot-tma"
+    assert comm.async_error() == 0
+    X.destroy()
+    C.destroy()
+    comm.destroy()
+    del dx, dc
+    wx, wc = O.easgd_async(xs, center, ALPHA, order)
+    for i in range(p):
+        assert_bitwise(got[i][0], wx[i], f"async x p={p} client {i}")
+        assert_bitwise(got[i][1], wc, f"async center p={p} replica {i}")

@@ -603,3 +603,59 @@ def test_group_cta_budget():
         g.set_num_ctas(-1)
     g.destroy()
     comm.destroy()
+
+
+# ------------------------------------------------------------------ NEXT row f2: async-server EASGD
+@pytest.mark.parametrize("c", [2, 3, 4, 8])
+@pytest.mark.parametrize("offset", [0, 1, "per-rank"])
+def test_easgd_async(c, offset):
+    """Server-side Elastic1 per arrival in a recorded order, Elastic2 at the client, bit-exact
+    vs oracle.easgd_async: ragged multi-tile groups, aligned / shifted / per-rank misaligned
+    tensors (vector, shifted and element paths), several orders."""
+    numels = [7, 13, 1000, 4096, 0, 2, 3001, 9000, 70001]
+    center = W.group(numels, "center", W.CFG_EASGD, 8, 0, W.CENTER)
+    xs = [W.client_params(numels, center, W.CFG_EASGD, 8, i) for i in range(c)]
+    g = np.random.default_rng(c)
+    off = (lambda k: k % 4) if offset == "per-rank" else (lambda k: offset)
+    for order in (None, list(reversed(range(c))), [int(i) for i in g.permutation(c)]):
+        comm = tc.Comm.emulated(c, 0)
+        dx = [to_dev(x, offset=off(i)) for i, x in enumerate(xs)]
+        dc = [to_dev(center, offset=off(i)) for i in range(c)]
+        X, C = tc.Group(comm, dx), tc.Group(comm, dc)
+        tc.easgd_async_update(X, C, 0.1, order)
+        assert comm.last_launch()[0] == "two-shot-tma"
+        assert comm.async_error() == 0
+        wx, wc = O.easgd_async(xs, center, 0.1, order)
+        for i in range(c):
+            assert_bitwise(to_host(dx[i]), wx[i], f"x client {i} order {order}")
+            assert_bitwise(to_host(dc[i]), wc, f"center replica {i} order {order}")
+        X.destroy()
+        C.destroy()
+        comm.destroy()
+
+
+def test_easgd_async_single_client_and_errors():
+    numels = [7, 13, 1000, 4099]
+    center = W.group(numels, "center", W.CFG_EASGD, 9, 0, W.CENTER)
+    x = W.client_params(numels, center, W.CFG_EASGD, 9, 0)
+    comm = tc.Comm.single(0)
+    dx, dc = to_dev(x), to_dev(center)
+    X, C = tc.Group(comm, dx), tc.Group(comm, dc)
+    tc.easgd_async_update(X, C, 0.25, [0])
+    wx, wc = O.easgd_async([x], center, 0.25)
+    assert_bitwise(to_host(dx), wx[0])
+    assert_bitwise(to_host(dc), wc)
+    X.destroy()
+    C.destroy()
+    comm.destroy()
+    comm = tc.Comm.emulated(3, 0)
+    dx = [to_dev(x) for _ in range(3)]
+    dc = [to_dev(center) for _ in range(3)]
+    X, C = tc.Group(comm, dx), tc.Group(comm, dc)
+    for bad in ([0, 0, 1], [0, 1, 3]):
+        with pytest.raises(tc.TcError) as e:
+            tc.easgd_async_update(X, C, 0.1, bad)
+        assert e.value.status == tc.tc.TC_ERR_INVALID_ARG
+    X.destroy()
+    C.destroy()
+    comm.destroy()

@@ -7,15 +7,16 @@
 
 A step is one pass of the hot path over one batch of synthetic gradients: tc_sgd_step =
 reduce-scatter + allgather of the whole ResNet-50 gradient group (161 tensors, 25.6 M fp32,
-102.2 MB per rank) fused with the SGD-momentum update (SURVEY.md §8(a) A2-A6), one kernel.
+102.2 MB per rank) fused with the SGD-momentum update (SURVEY.md §8(a) A1-A6), one kernel.
 Each step's gradients are fresh (copied in from a pristine buffer before the step, as a backward
 pass would write them); the copy is outside the timed kernel.  Inputs (3 groups, 307 MB per
 GPU) exceed the 126 MB L2, so no L2 flush is needed.
 
-value = all ranks' gradient bytes reduced per second = N * S / t_step  (GB/s).  The BASELINE
-"bus GB/s" (nccl-tests convention, 2(p-1)/p * S / t per rank) is reported as busbw_gbs and is the
-roofline's achieved figure for N >= 2 (bound: NVLink).  At N = 1 there is no communication and
-the roofline is HBM (5 S bytes per step).  Rank 0 prints ONE JSON line.
+value (BASELINE.json metric):
+  N >= 2: the step's bus bandwidth, busbw = 2(N-1)/N * S / t (nccl-tests convention; the
+          paper's bandwidth term, P:331), the roofline's achieved figure (bound: NVLink);
+  N = 1:  no communication -- the fused step's HBM bandwidth 5S / t (bound: HBM).
+whole_job_gbs = N * S / t is reported beside it.  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -34,8 +35,8 @@ import numpy as np  # noqa: E402
 
 import tc_workloads as W  # noqa: E402
 
-METRIC = ("tensor-allreduce + fused SGD-momentum step, gradient GB/s reduced (N*S/t; "
-          "busbw_gbs = BASELINE bus GB/s), ResNet-50 grad group")
+METRIC = ("tensor-allreduce bus GB/s of the fused allreduce + SGD-momentum step, ResNet-50 grad "
+          "group (N>=2: busbw = 2(N-1)/N*S/t; N=1: HBM GB/s of the step, 5S/t)")
 UNIT = "GB/s"
 NVLINK_PEER_GBS = 770.0     # B200_PROFILING.md: measured peer copy per direction (900 nominal)
 NVLINK_NOMINAL_GBS = 900.0
@@ -141,64 +142,159 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
-# ------------------------------------------------------------------ CPU oracle baseline
-def cpu_baseline_sgd(numels, p, budget_s=12.0, max_steps=20):
-    """The oracle as it stands (numpy, one thread) on the same workload: sgd_step over p
-    simulated ranks.  Bounded: the full group when it fits the time budget, else a contiguous
-    prefix of the group's tensors."""
+
+
+# ------------------------------------------------------------------ CPU oracle (baselines)
+# The oracle as it stands: oracle.sgd_step over p simulated ranks.  Its arithmetic is
+# elementwise within each tensor, so the all-cores baseline runs the same function on contiguous
+# slices of the flattened group in a multiprocessing pool ("a multiprocessing
+# pool over contiguous flat-space slices, len(os.sched_getaffinity(0)) workers"); the inputs
+# live in shared memory.
+_POOL = {}
+
+
+def _pool_sgd(ab):
     from oracle import tc_oracle as O
-    gs = [W.group(numels, "grad", W.CFG_RESNET50, 0, k, W.GRAD) for k in range(p)]
-    w = W.group(numels, "param", W.CFG_RESNET50, 0, 0, W.PARAM)
-    dw = W.group(numels, "dw", W.CFG_RESNET50, 0, 0, W.DW)
-    hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
-    t0 = time.perf_counter()
-    steps = 0
-    while steps < max_steps and (time.perf_counter() - t0) < budget_s:
-        O.sgd_step([w] * p, gs, [dw] * p, **hp)
-        steps += 1
-    dt = (time.perf_counter() - t0) / steps
+    a, b = ab
+    st = _POOL
+    G, Ws, Ds = O.sgd_step([[st["w"][a:b]]], [[g[a:b]] for g in st["g"]], [[st["dw"][a:b]]],
+                           **st["hp"])
+    st["G_out"][a:b] = G[0]
+    st["w_out"][a:b] = Ws[0][0]
+    st["dw_out"][a:b] = Ds[0][0]
+    return b - a
+
+
+class OracleSGD:
+    """The p-rank fused step of config 2 on the host: inputs generated from the same seeds as
+    the GPU run (rank k's gradient group, the replicated w and dw), flattened."""
+
+    def __init__(self, numels, p, cfg=W.CFG_RESNET50):
+        from multiprocessing import shared_memory
+        self.numels, self.p = numels, p
+        self.N = int(sum(numels))
+        self.hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
+        self._shm = []
+
+        def shared(fill=None):
+            m = shared_memory.SharedMemory(create=True, size=4 * self.N)
+            self._shm.append(m)
+            a = np.ndarray((self.N,), np.float32, buffer=m.buf)
+            if fill is not None:
+                a[:] = np.concatenate(fill)
+            return a
+
+        self.g = [shared(W.group(numels, "grad", cfg, 0, k, W.GRAD)) for k in range(p)]
+        self.w = shared(W.group(numels, "param", cfg, 0, 0, W.PARAM))
+        self.dw = shared(W.group(numels, "dw", cfg, 0, 0, W.DW))
+        self.outs = [shared() for _ in range(3)]
+        self.pool = None
+        self.cores = 1
+
+    def step_single(self):
+        """One thread: the oracle over the whole group, as the tests call it."""
+        from oracle import tc_oracle as O
+        O.sgd_step([[self.w]], [[g] for g in self.g], [[self.dw]], **self.hp)
+
+    def start_pool(self):
+        import multiprocessing as mp
+        self.cores = len(os.sched_getaffinity(0))
+        _POOL.update(g=self.g, w=self.w, dw=self.dw, hp=self.hp, G_out=self.outs[0],
+                     w_out=self.outs[1], dw_out=self.outs[2])
+        self.pool = mp.get_context("fork").Pool(self.cores)
+        n = 4 * self.cores
+        cuts = [self.N * i // n for i in range(n + 1)]
+        self.slices = [(cuts[i], cuts[i + 1]) for i in range(n) if cuts[i + 1] > cuts[i]]
+
+    def step_pool(self):
+        assert sum(self.pool.map(_pool_sgd, self.slices)) == self.N
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+        for m in self._shm:
+            m.close()
+            m.unlink()
+
+
+def step_value(p, S, t_s):
+    """The BASELINE metric of one step of t_s seconds: busbw (p >= 2) or 5S/t (p = 1)."""
+    return (2 * (p - 1) / p * S if p > 1 else 5 * S) / t_s / 1e9
+
+
+def workload_config(config, numels, p):
+    """The `config` object, identical in both arms (the reference arm runs the same workload)."""
     S = 4 * sum(numels)
-    return {"value": p * S / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"full group ({len(numels)} tensors, {S/1e6:.1f} MB/rank) x {p} ranks, "
-                      f"{steps} oracle steps, {dt:.3f} s/step"}
+    return {"workload": f"{config} gradient group: allreduce + fused SGD-momentum step "
+                        f"(tc_sgd_step), {len(numels)} tensors, {S/1e6:.2f} MB per rank",
+            "global_batch": None, "p": p, "parallelism": f"dp{p}",
+            "hyper": "lr 0.1, momentum 0.9, wd 1e-4, rescale 1/(128 p)",
+            "l2": "inputs larger than L2 (3 groups, %.0f MB per GPU); no flush" % (3 * S / 1e6)}
+
+
+def cpu_baseline_sgd(numels, p, budget_s=20.0):
+    """Our arm's cpu_baseline (rank 0, N = 1): the oracle on the same workload, bounded to about
+    `budget_s` of CPU work -- one thread, then all cores."""
+    o = OracleSGD(numels, p)
+    S = 4 * sum(numels)
+    try:
+        t0 = time.perf_counter()
+        n1 = 0
+        while n1 < 3 and time.perf_counter() - t0 < budget_s / 2:
+            o.step_single()
+            n1 += 1
+        t1 = (time.perf_counter() - t0) / n1
+        o.start_pool()
+        o.step_pool()  # warm the workers
+        t0 = time.perf_counter()
+        nall = 0
+        while nall < 20 and time.perf_counter() - t0 < budget_s / 2:
+            o.step_pool()
+            nall += 1
+        tall = (time.perf_counter() - t0) / nall
+    finally:
+        o.close()
+    desc = f"full group ({len(numels)} tensors, {S/1e6:.1f} MB/rank) x {p} ranks per step"
+    return {"value": step_value(p, S, tall), "unit": UNIT, "cores": o.cores, "kind": "oracle",
+            "sample": f"{desc}; all cores: {nall} steps, {tall:.3f} s/step",
+            "single_thread": {"value": step_value(p, S, t1), "cores": 1,
+                              "sample": f"{desc}; {n1} steps, {t1:.3f} s/step"}}
 
 
 # ------------------------------------------------------------------ the reference arm
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle as it stands, on our arm's workload (the whole
+    p-rank fused step on the full group every step), on all host cores of rank 0."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle import tc_oracle as O
     p = max(args.gpus, 1)
     numels = W.GROUPS[args.config]
-    # bounded sample per step: a prefix of the group of at most 4 M elements
-    sample, tot = [], 0
-    for n in numels:
-        if tot + n > 4_000_000 and sample:
-            break
-        sample.append(n)
-        tot += n
-    gs = [W.group(sample, "grad", W.CFG_RESNET50, 0, k, W.GRAD) for k in range(p)]
-    w = W.group(sample, "param", W.CFG_RESNET50, 0, 0, W.PARAM)
-    dw = W.group(sample, "dw", W.CFG_RESNET50, 0, 0, W.DW)
-    hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
-    for _ in range(args.warmup):
-        O.sgd_step([w] * p, gs, [dw] * p, **hp)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        O.sgd_step([w] * p, gs, [dw] * p, **hp)
-    dt = (time.perf_counter() - t0) / args.steps
-    S = 4 * tot
-    v = p * S / dt / 1e9
-    desc = (f"prefix of {len(sample)} of {len(numels)} {args.config} tensors ({S/1e6:.1f} MB/rank) "
-            f"x {p} simulated ranks per step")
+    S = 4 * sum(numels)
+    o = OracleSGD(numels, p)
+    try:
+        o.start_pool()
+        for _ in range(args.warmup):
+            o.step_pool()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            o.step_pool()
+        dt = (time.perf_counter() - t0) / args.steps
+    finally:
+        o.close()
+    v = step_value(p, S, dt)
+    desc = (f"full {args.config} group ({len(numels)} tensors, {S/1e6:.1f} MB/rank) x {p} "
+            f"simulated ranks every step, {o.cores} worker processes over flat slices")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": f"{args.config} grad group, oracle sgd_step",
-                                        "p": p, "sample": desc},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "data": "synthetic (seeded; torchvision ResNet-50 parameter shapes, SURVEY.md App. A)",
+        "config": workload_config(args.config, numels, p),
+        "whole_job_gbs": p * S / dt / 1e9,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": o.cores, "kind": "oracle",
+                         "sample": desc},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -261,18 +357,38 @@ def config4_sequence(args, p, rank, local, numels, dev, ecomm, cen, stream, time
     return out
 
 
+def nccl_allreduce_us(flat, stream, warmup, K, world, group=None):
+    import torch
+    import torch.distributed as dist
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            dist.all_reduce(flat, group=group)
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            dist.all_reduce(flat, group=group)
+        e1.record(stream)
+        stream.synchronize()
+    return max_over_ranks(e0.elapsed_time(e1) / K, world) * 1e3
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="tc", choices=["tc", "reference"])
     ap.add_argument("--config", default="resnet50", choices=["resnet50", "alexnet", "vgg16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="only the step (and e2e): skip allreduce/broadcast/NCCL/EASGD/config-4")
     ap.add_argument("--algo", type=int, default=0,
-                    help="0 auto, 1 two-shot pull, 3 two-shot push, 4 NVLS")
+                    help="0 auto, 1 two-shot pull, 3 two-shot push, 4 NVLS, 6 TMA, 7 balanced")
+    ap.add_argument("--switch", action="store_true",
+                    help="let the automatic choice use NVLS (tc_comm_set_switch_reduction)")
     ap.add_argument("--no-sym", action="store_true",
                     help="keep gradients in torch memory (no NVLS) instead of tc_mem_alloc")
     args = ap.parse_args()
@@ -293,21 +409,25 @@ def main():
     S = 4 * sum(numels)
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (p * 128))
     stream = torch.cuda.Stream()
+
     def dev(grp):
         """The group's tensors as views of one flat allocation (a gradient bucket, as frameworks
         lay them out); libtc still receives T separate pointers and assumes nothing."""
         flat = torch.from_numpy(np.concatenate(grp)).cuda()
         return flat, list(torch.split(flat, [int(n) for n in numels]))
 
-    gp_flat, g_pristine = dev(W.group(numels, "grad", W.CFG_RESNET50, 0, rank, W.GRAD))
+    cfg_id = W.CFG_RESNET50
+    gp_flat, _ = dev(W.group(numels, "grad", cfg_id, 0, rank, W.GRAD))
     g_flat, g = dev(W.group(numels, "zeros", 0, 0, 0, 0))
     g_flat.copy_(gp_flat)
-    w_flat, w = dev(W.group(numels, "param", W.CFG_RESNET50, 0, 0, W.PARAM))
-    dw_flat, dw = dev(W.group(numels, "dw", W.CFG_RESNET50, 0, 0, W.DW))
+    w_flat, w = dev(W.group(numels, "param", cfg_id, 0, 0, W.PARAM))
+    dw_flat, dw = dev(W.group(numels, "dw", cfg_id, 0, 0, W.DW))
     torch.cuda.synchronize()
 
     comm = tc.Comm.single(local) if p == 1 else tc.Comm.from_process_group(device=local)
     comm.set_algorithm(args.algo)
+    if args.switch:
+        comm.set_switch_reduction(True)
     sym = p > 1 and not args.no_sym
     if sym:
         # the gradient bucket in symmetric multicast memory (tc_mem_alloc): NVLS-eligible
@@ -357,9 +477,8 @@ def main():
     t_ms = max_over_ranks(kernel_ms, world)
     algo, ctas, threads = comm.last_launch()
     t_s = t_ms / 1e3
-    value = p * S / t_s / 1e9
+    value = step_value(p, S, t_s)
     algbw = S / t_s / 1e9
-    busbw = algbw * 2 * (p - 1) / p if p > 1 else 0.0
     hbm_peak, hbm_src = peaks()
     traffic = None
     try:
@@ -371,72 +490,84 @@ def main():
         hbm_bytes = 5 * S  # read g, w, dw; write w, dw
         roofline = {"bound": "hbm", "achieved": hbm_bytes / t_s / 1e9, "peak": hbm_peak,
                     "unit": "GB/s", "frac": hbm_bytes / t_s / 1e9 / hbm_peak, "traffic": traffic,
-                    "peak_source": hbm_src, "algorithmic_bytes_per_launch": hbm_bytes}
+                    "achieved_is": "algorithmic bytes (5S) / CUDA-event time of the step kernel",
+                    "peak_source": hbm_src, "algorithmic_bytes_per_launch": hbm_bytes,
+                    "kernel": "k_local_tma<OP_SGD>"}
     else:
         nvl_bytes = 2 * (p - 1) / p * S
-        roofline = {"bound": "nvlink", "achieved": busbw, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
-                    "frac": busbw / NVLINK_PEER_GBS, "frac_of_nominal_900": busbw / NVLINK_NOMINAL_GBS,
+        roofline = {"bound": "nvlink", "achieved": value, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                    "frac": value / NVLINK_PEER_GBS, "frac_of_nominal_900": value / NVLINK_NOMINAL_GBS,
                     "traffic": traffic,
+                    "achieved_is": "algorithmic NVLink bytes per GPU 2(p-1)/p S / CUDA-event time",
                     "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
-                    "algorithmic_bytes_per_launch": nvl_bytes}
+                    "algorithmic_bytes_per_launch": nvl_bytes, "kernel": f"{algo} (OP_SGD)"}
 
     extra = {}
-    # allreduce alone (scale 1/p keeps the values fixed from call to call)
-    if p > 1:
-        with torch.cuda.stream(stream):
-            for _ in range(args.warmup):
-                tc.allreduce(G, 1.0 / p, stream=stream)
-            barrier(world)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(K):
-                tc.allreduce(G, 1.0 / p, stream=stream)
-            e1.record(stream)
-            stream.synchronize()
-        ta = max_over_ranks(e0.elapsed_time(e1) / K, world) / 1e3
-        extra["allreduce_only"] = {"t_us": ta * 1e6, "busbw_gbs": S / ta / 1e9 * 2 * (p - 1) / p,
+    if p > 1 and not args.no_extras:
+        def timed_us(fn):
+            with torch.cuda.stream(stream):
+                for _ in range(args.warmup):
+                    fn()
+                barrier(world)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(K):
+                    fn()
+                e1.record(stream)
+                stream.synchronize()
+            return max_over_ranks(e0.elapsed_time(e1) / K, world) * 1e3
+
+        # allreduce alone (scale 1/p keeps the values fixed from call to call)
+        ta = timed_us(lambda: tc.allreduce(G, 1.0 / p, stream=stream))
+        extra["allreduce_only"] = {"t_us": ta, "busbw_gbs": 2 * (p - 1) / p * S / ta / 1e3,
                                    "algo": comm.last_launch()[0]}
+        if sym and comm.multicast_supported:
+            comm.set_algorithm(4)
+            tn = timed_us(lambda: tc.allreduce(G, 1.0 / p, stream=stream))
+            extra["allreduce_nvls"] = {"t_us": tn, "busbw_gbs": 2 * (p - 1) / p * S / tn / 1e3,
+                                       "link_gbs_per_dir": (1 + 1 / p) * S / tn / 1e3,
+                                       "note": "algorithm 4 (switch reduction, fp32 in the "
+                                               "switch: tolerance contract)"}
+            comm.set_algorithm(args.algo)
         # tensor broadcast from rank 0 (weight initialisation): scatter + allgather
-        with torch.cuda.stream(stream):
-            for _ in range(args.warmup):
-                tc.broadcast(G, 0, stream=stream)
-            barrier(world)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(K):
-                tc.broadcast(G, 0, stream=stream)
-            e1.record(stream)
-            stream.synchronize()
-        tb = max_over_ranks(e0.elapsed_time(e1) / K, world) / 1e3
-        extra["broadcast"] = {"t_us": tb * 1e6, "algbw_gbs": S / tb / 1e9,
-                              "busbw_gbs": S / tb / 1e9 * (p - 1) / p,
+        tb = timed_us(lambda: tc.broadcast(G, 0, stream=stream))
+        extra["broadcast"] = {"t_us": tb, "algbw_gbs": S / tb / 1e3,
+                              "busbw_gbs": S / tb / 1e3 * (p - 1) / p,
                               "algo": comm.last_launch()[0]}
         if not args.no_nccl:
             import torch.distributed as dist
             flat = torch.empty(sum(numels), dtype=torch.float32, device="cuda")
             flat.normal_()
-            with torch.cuda.stream(stream):
-                for _ in range(args.warmup):
-                    dist.all_reduce(flat)
-                barrier(world)
-                e0.record(stream)
-                for _ in range(K):
-                    dist.all_reduce(flat)
-                e1.record(stream)
-                stream.synchronize()
-            tn = max_over_ranks(e0.elapsed_time(e1) / K, world) / 1e3
-            extra["nccl_allreduce_flat"] = {"t_us": tn * 1e6,
-                                            "busbw_gbs": S / tn / 1e9 * 2 * (p - 1) / p,
+            tn = nccl_allreduce_us(flat, stream, args.warmup, K, world)
+            extra["nccl_allreduce_flat"] = {"t_us": tn, "busbw_gbs": 2 * (p - 1) / p * S / tn / 1e3,
                                             "note": "torch.distributed NCCL all_reduce on one flat "
-                                                    "buffer of N fp32 (comparison only)"}
+                                                    "buffer of N fp32, default algorithm "
+                                                    "(comparison only)"}
+            # NCCL_ALGO is read when a communicator is created: a new group created with it set
+            old = os.environ.get("NCCL_ALGO")
+            os.environ["NCCL_ALGO"] = "Ring"
+            ring = dist.new_group(backend="nccl")
+            dist.all_reduce(flat, group=ring)  # creates the ring communicator now
+            torch.cuda.synchronize()
+            if old is None:
+                del os.environ["NCCL_ALGO"]
+            else:
+                os.environ["NCCL_ALGO"] = old
+            tr = nccl_allreduce_us(flat, stream, args.warmup, K, world, group=ring)
+            extra["nccl_ring_allreduce_flat"] = {
+                "t_us": tr, "busbw_gbs": 2 * (p - 1) / p * S / tr / 1e3,
+                "note": "NCCL with NCCL_ALGO=Ring at communicator creation (the paper's ring "
+                        "design (b), P:504), same flat buffer"}
+            dist.destroy_process_group(ring)
             del flat
 
     # EASGD update (A7) on the ResNet-50 params: pairs (k, k + N/2) as in config 4
     _, x_c = dev(W.group(numels, "param", W.CFG_EASGD, 0, 0, W.PARAM))
     _, cen = dev(W.group(numels, "center", W.CFG_EASGD, 0, 0, W.CENTER))
+    ecomm = None
     if p == 1:
         ecomm = comm
-    else:
+    elif not args.no_extras:
         import torch.distributed as dist
         mine = None
         if p % 2 == 0:
@@ -448,32 +579,8 @@ def main():
         else:
             mine = dist.new_group(backend="gloo")
         ecomm = tc.Comm.from_process_group(mine, device=local) if mine is not None else None
-    if ecomm is not None:
+    if ecomm is not None and not args.no_extras:
         X, C = tc.Group(ecomm, x_c), tc.Group(ecomm, cen)
-        with torch.cuda.stream(stream):
-            for _ in range(args.warmup):
-                tc.easgd_update(X, C, 0.1, stream=stream)
-            barrier(world)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(K):
-                tc.easgd_update(X, C, 0.1, stream=stream)
-            e1.record(stream)
-            stream.synchronize()
-        te = max_over_ranks(e0.elapsed_time(e1) / K, world) / 1e3
-        c = ecomm.nranks
-        extra["easgd"] = {"t_us": te * 1e6, "clients": c,
-                          "nvlink_ingress_gbs": (c - 1) * S / te / 1e9 if c > 1 else 0.0,
-                          "hbm_gbs_local": 4 * S / te / 1e9 if c == 1 else None,
-                          "algo": ecomm.last_launch()[0]}
-        # NEXT row f2: the same update fused with each client's own SGD step (tc_esgd_step),
-        # against the separate calls (tc_easgd_update + a local tc_sgd_step)
-        _, g_c = dev(W.group(numels, "grad", W.CFG_EASGD, 1, rank, W.GRAD))
-        _, d_c = dev(W.group(numels, "dw", W.CFG_EASGD, 2, rank, W.DW))
-        Gc, Dc = tc.Group(ecomm, g_c), tc.Group(ecomm, d_c)
-        lcomm = comm if p == 1 else tc.Comm.single(local)
-        Wl, Gl, Dl = tc.Group(lcomm, x_c), tc.Group(lcomm, g_c), tc.Group(lcomm, d_c)
-        ehp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 128)
 
         def timed_calls(fn):
             with torch.cuda.stream(stream):
@@ -488,6 +595,26 @@ def main():
                 stream.synchronize()
             return max_over_ranks(a0.elapsed_time(a1) / K, world) * 1e3
 
+        te = timed_calls(lambda: tc.easgd_update(X, C, 0.1, stream=stream))
+        c = ecomm.nranks
+        extra["easgd"] = {"t_us": te, "clients": c,
+                          "nvlink_ingress_gbs": (c - 1) * S / te / 1e3 if c > 1 else 0.0,
+                          "hbm_gbs_local": 4 * S / te / 1e3 if c == 1 else None,
+                          "algo": ecomm.last_launch()[0]}
+        if c > 1:
+            order = list(reversed(range(c)))
+            tas = timed_calls(lambda: tc.easgd_async_update(X, C, 0.1, order, stream=stream))
+            extra["easgd_async"] = {"t_us": tas, "clients": c, "order": order,
+                                    "algo": ecomm.last_launch()[0],
+                                    "note": "NEXT row f2: server-side Elastic1 per arrival"}
+        # NEXT row f2: the same update fused with each client's own SGD step (tc_esgd_step),
+        # against the separate calls (tc_easgd_update + a local tc_sgd_step)
+        _, g_c = dev(W.group(numels, "grad", W.CFG_EASGD, 1, rank, W.GRAD))
+        _, d_c = dev(W.group(numels, "dw", W.CFG_EASGD, 2, rank, W.DW))
+        Gc, Dc = tc.Group(ecomm, g_c), tc.Group(ecomm, d_c)
+        lcomm = comm if p == 1 else tc.Comm.single(local)
+        Wl, Gl, Dl = tc.Group(lcomm, x_c), tc.Group(lcomm, g_c), tc.Group(lcomm, d_c)
+        ehp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 128)
         t_fused = timed_calls(lambda: tc.esgd_step(X, C, Gc, Dc, 0.1, stream=stream, **ehp))
         t_sep = timed_calls(lambda: (tc.easgd_update(X, C, 0.1, stream=stream),
                                      tc.sgd_step(Wl, Gl, Dl, stream=stream, **ehp)))
@@ -504,8 +631,8 @@ def main():
                                                 stream, timed_calls)
         X.destroy()
         C.destroy()
-        if ecomm is not comm:
-            ecomm.destroy()
+    if ecomm is not None and ecomm is not comm:
+        ecomm.destroy()
 
     # e2e through the public API with host buffers: pinned H2D of the step's gradients,
     # tc_sgd_step, D2H of the updated parameters.
@@ -561,8 +688,8 @@ def main():
             e1.record(stream)
             stream.synchronize()
         tt = max_over_ranks(e0.elapsed_time(e1) / Ke, world) / 1e3
-        e2e = {"value": p * S / tt / 1e9, "unit": UNIT, "h2d_bytes_per_step": S,
-               "d2h_bytes_per_step": S, "ms_per_step": tt * 1e3,
+        e2e = {"value": step_value(p, S, tt), "unit": UNIT, "h2d_bytes_per_step": S,
+               "d2h_bytes_per_step": S, "ms_per_step": tt * 1e3, "whole_job_gbs": p * S / tt / 1e9,
                "pipelining": "H2D of step i+1 overlaps step i's kernel and D2H"}
         groups[1].destroy()
         if sym:
@@ -577,13 +704,12 @@ def main():
         "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded; torchvision ResNet-50 parameter shapes, SURVEY.md App. A)",
-        "config": {"workload": f"{args.config} gradient group: tc_sgd_step (allreduce + fused "
-                               f"SGD-momentum), {len(numels)} tensors, {S/1e6:.2f} MB per rank",
-                   "global_batch": None, "p": p, "algo": algo, "ctas": ctas, "threads": threads,
+        "config": workload_config(args.config, numels, p),
+        "launch": {"algo": algo, "ctas": ctas, "threads": threads,
                    "grad_memory": "tc_mem_alloc (symmetric, multicast)" if sym else "torch",
-                   "l2": "inputs larger than L2 (3 groups, %.0f MB per GPU); no flush" % (3 * S / 1e6),
-                   "parallelism": f"dp{p}"},
-        "busbw_gbs": busbw, "algbw_gbs": algbw, "t_us": t_ms * 1e3,
+                   "switch_reduction_allowed": bool(args.switch)},
+        "whole_job_gbs": p * S / t_s / 1e9, "busbw_gbs": value if p > 1 else 0.0,
+        "algbw_gbs": algbw, "t_us": t_ms * 1e3,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": K, "clocks": clocks.summary(), "wall_s_timed_region": t_wall,
     }

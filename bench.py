@@ -528,7 +528,25 @@ def main():
                                        "link_gbs_per_dir": (1 + 1 / p) * S / tn / 1e3,
                                        "note": "algorithm 4 (switch reduction, fp32 in the "
                                                "switch: tolerance contract)"}
+            # the fused step on the switch (fresh gradients before every kernel, as the step)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(K)]
+            with torch.cuda.stream(stream):
+                for i in range(args.warmup + K):
+                    refresh_g()
+                    if i >= args.warmup:
+                        evs[i - args.warmup][0].record(stream)
+                    step()
+                    if i >= args.warmup:
+                        evs[i - args.warmup][1].record(stream)
+                stream.synchronize()
+            ts = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / K, world) * 1e3
+            extra["sgd_step_nvls"] = {"t_us": ts, "busbw_gbs": 2 * (p - 1) / p * S / ts / 1e3,
+                                      "algo": comm.last_launch()[0],
+                                      "note": "tc_sgd_step on algorithm 4: switch reduction, "
+                                              "HBM epilogue overlapped per published round"}
             comm.set_algorithm(args.algo)
+            refresh_g()
         # tensor broadcast from rank 0 (weight initialisation): scatter + allgather
         tb = timed_us(lambda: tc.broadcast(G, 0, stream=stream))
         extra["broadcast"] = {"t_us": tb, "algbw_gbs": S / tb / 1e3,

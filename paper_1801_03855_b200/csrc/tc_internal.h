@@ -18,7 +18,7 @@ namespace tc {
 
 constexpr int kMaxRanks = TC_MAX_RANKS;
 constexpr int kMaxCtas = 1024;                 // per barrier and source rank
-constexpr int kNumBarriers = 3;                // entry, mid, exit
+constexpr int kNumBarriers = 3;                // entry, mid, NVLS progress
 constexpr size_t kFlagWords = (size_t)kNumBarriers * kMaxRanks * kMaxCtas;
 constexpr size_t kStageCapacity = 8u << 20;    // one-shot staging bytes per parity
 constexpr size_t kLLBytes = 16u << 20;         // low-latency receive buffers (after staging)
@@ -84,7 +84,8 @@ constexpr int t2_smem(int op, int p) {
   return t2_stages(op, p) * t2_ops(op, p) * t2_slots(p) * 16;
 }
 
-enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_EXIT = 2 };
+constexpr int kNvlsThreads = 512;              // NVLS: 16 warps (reduction / signal / epilogue)
+enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_PROG = 2 };  // PROG: NVLS round progress
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4, OP_EASYNC = 5 };
 enum Algo {
   ALGO_LOCAL = 0,

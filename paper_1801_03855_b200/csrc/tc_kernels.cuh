@@ -655,72 +655,6 @@ __device__ __forceinline__ bool gather_all(const KParams& kp, int r, int par) {
   return true;
 }
 
-// ------------------------------------------------------------------ NVLS (switch reduction)
-// multimem.ld_reduce on a multicast address returns the sum of every rank's copy, reduced in
-// the NVSwitch (fp32, order chosen by the switch); multimem.st writes every rank's copy.
-__device__ __forceinline__ float4 mm_ld_reduce16(const float* p) {
-  float4 v;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ float mm_ld_reduce4(const float* p) {
-  float v;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void mm_st16(float* p, float4 v) {
-  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void mm_st4(float* p, float v) {
-  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
-// Owner side of NVLS: reduce every rank's copy of an owned slot in the switch, apply the
-// allreduce scale, multicast-store the result into every rank's copy.
-template <int OP>
-struct NvlsBody {
-  static constexpr int NP = 1;
-  const KParams& kp;
-  int r;
-  struct State {
-    float4 v;
-    float* mp;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const { ptr[0] = kp.mc[t]; }
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
-    st.mp = ptr[0] + ref.e;
-    if constexpr (VEC) {
-      st.v = mm_ld_reduce16(st.mp);
-    } else {
-      st.v = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i >= ref.lo_i && i < ref.hi_i) lane(st.v, i) = mm_ld_reduce4(st.mp + i);
-    }
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-    if constexpr (OP == OP_ALLREDUCE) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        lane(st.v, i) = __double2float_rn(__dmul_rn((double)lane(st.v, i), (double)kp.scale));
-    }
-    if constexpr (VEC) {
-      mm_st16(st.mp, st.v);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i >= ref.lo_i && i < ref.hi_i) mm_st4(st.mp + i, lane(st.v, i));
-    }
-  }
-};
-
 // ------------------------------------------------------------------ low-latency (LL)
 // Rank r's words for peer k live in k's LL buffer [parity][source r][4*slot + lane]: 8 bytes =
 // {epoch, value bits}.  8-byte stores are single-copy atomic, so a reader that sees the current
@@ -913,49 +847,6 @@ __global__ void __launch_bounds__(512, MINB) k_ll(KParams kp) {
   stamp(kp, 0);
   LLBody<OP, P> body{kp, r, (int)(ep() & 1u)};
   slot_loop_flat(kp, 0, kp.M, body);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
-// NVLS: ENTRY barrier -> owner slots reduced in the switch and multicast back -> MID barrier
-// (every owner's stores landed everywhere) -> SGD epilogue over this CTA's pieces of every
-// chunk from local memory.  Per GPU: ~(1 + 1/p) S of NVLink traffic each way.
-template <int OP, int P, int MINB>
-__global__ void __launch_bounds__(512, MINB) k_nvls(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  const int64_t M = kp.M;
-  stamp(kp, 0);
-  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
-  stamp(kp, 1);
-  {
-    NvlsBody<OP> body{kp, r};  // small state: 4 switch reductions in flight per lane
-    slot_loop<4>(kp, (int)(M * r / P), (int)(M * (r + 1) / P), body);
-  }
-  __threadfence_system();
-  stamp(kp, 2);
-  if constexpr (OP == OP_SGD) {
-    // epilogue: my own chunk first, then every other chunk as soon as its owner's CTA is done
-    signal_all(kp, r, BAR_MID);
-    auto epi = [&](int q) {
-      ReduceBody<OP_SGD, 1, SRC_TENSORS, false> body{kp, r, 0, nullptr};
-      slot_loop<unroll_for(1, MINB)>(kp, (int)(M * q / P), (int)(M * (q + 1) / P), body);
-    };
-    epi(r);
-    stamp(kp, 3);
-#pragma unroll 1
-    for (int j = 0; j < P - 1; ++j) {
-      const int q = (r + 1 + j) % P;
-      if (!wait_one(kp, r, q, BAR_MID)) return;
-      epi(q);
-    }
-  } else {
-    // the result must have landed everywhere before the kernel (the call) completes
-    if (!barrier_all(kp, r, BAR_MID, true)) return;
-    stamp(kp, 3);
-  }
-  stamp(kp, 4);
   call_end(kp, r);
   stamp(kp, 5);
 }
@@ -1749,13 +1640,236 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_bal(KParams kp) {
   stamp(kp, 5);
 }
 
+// ------------------------------------------------------------------ NVLS (switch reduction)
+// The owner of a chunk reads every rank's copy of it reduced in the NVSwitch
+// (multimem.ld_reduce on the multicast address: fp32 sums in the switch's order) and writes the
+// result into every rank's copy with one multimem.st.  Per GPU: egress S (serving every owner's
+// reductions) + S/p, ingress S/p + S -- (1 + 1/p) S each way against the two-shot's 2(p-1)/p S.
+//
+// Work: the owner chunk's tiles (the TMA two-shot's table: runs of <= 512 slots inside one
+// tensor), tile i of a chunk on CTA i mod grid on every rank.  Inside a CTA the NVLS warps take
+// the CTA's tiles round-robin, a round = one tile per NVLS warp (more when a CTA holds > 255
+// rounds).  When every NVLS warp has reached the end of a round (named barrier 1), the signal
+// warp fences at system scope and stores the round count into every rank's progress flag
+// [BAR_PROG][this rank][this CTA].  Consumers on every rank (CTA b waits for CTA b of owner q):
+//   SGD       -- the epilogue warps apply the update to round j's tiles of chunk q as soon as
+//                owner q published round j: G (the stored sum) is written back already, w and
+//                dw are updated from local memory -- the HBM epilogue overlaps the switch work;
+//   allreduce -- the signal warp waits for every owner's last round (the call must not complete
+//                before every owner's stores have landed here).
+__device__ __forceinline__ float4 mm_ld_reduce16(const float* p) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float mm_ld_reduce4(const float* p) {
+  float v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mm_st16(float* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st4(float* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+constexpr int kNvlsWarps = kNvlsThreads / 32;
+__host__ __device__ constexpr int nvls_reduce_warps(int op) { return op == OP_ALLREDUCE ? 12 : 6; }
+
+// A tile of owner q's chunk as seen by this rank: element offset e of its first slot inside
+// tensor t (negative for a shifted head), slot count n, vector path when the tile is whole
+// 16-B slots.
+struct NvTile {
+  int t, n;
+  int64_t e;
+  bool full;
+};
+__device__ __forceinline__ NvTile nv_tile(const KParams& kp, int gi) {
+  const int4 tl = kp.tiles2[gi];
+  NvTile d;
+  d.t = tl.x;
+  d.n = tl.z;
+  d.e = (int64_t)(tl.y - kp.prefix[d.t]) * 4 - kp.shift[d.t];
+  d.full = d.e >= 0 && d.e + 4 * (int64_t)d.n <= kp.numel[d.t];
+  return d;
+}
+
+// Tiles of owner q's chunk held by this CTA, and the tiles per round.
+__device__ __forceinline__ void nv_counts(const KParams& kp, int q, int nw, int& cnt, int& tpr) {
+  const int n = kp.tile2_off[q + 1] - kp.tile2_off[q];
+  const int b = (int)blockIdx.x, G = (int)gridDim.x;
+  cnt = n > b ? (n - b + G - 1) / G : 0;
+  const int m = (cnt + 255 * nw - 1) / (255 * nw);
+  tpr = nw * (m > 0 ? m : 1);
+}
+__device__ __forceinline__ uint32_t nv_flag_value(int rounds) {
+  return (ep() << 8) | (uint32_t)rounds;
+}
+
+// Whole warp: switch-reduce one tile of this rank's chunk and multicast the result.
+template <int OP>
+__device__ __forceinline__ void nv_reduce_tile(const KParams& kp, const NvTile& d, int lane_id) {
+  float* mc = kp.mc[d.t] + d.e;
+  const bool vec = d.full && (((uintptr_t)mc & 15) == 0);
+  auto fin = [&](float v) {
+    return OP == OP_ALLREDUCE ? __double2float_rn(__dmul_rn((double)v, (double)kp.scale)) : v;
+  };
+  if (vec) {
+    constexpr int U = 4;
+    for (int s0 = lane_id; s0 < d.n; s0 += 32 * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + 32 * u < d.n) v[u] = mm_ld_reduce16(mc + 4 * (s0 + 32 * u));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (s0 + 32 * u >= d.n) continue;
+        v[u] = make_float4(fin(v[u].x), fin(v[u].y), fin(v[u].z), fin(v[u].w));
+        mm_st16(mc + 4 * (s0 + 32 * u), v[u]);
+      }
+    }
+  } else {
+    const int64_t j0 = d.e < 0 ? -d.e : 0;
+    const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
+    for (int64_t j = j0 + lane_id; j < j1; j += 32) mm_st4(mc + j, fin(mm_ld_reduce4(mc + j)));
+  }
+}
+
+// Whole warp: the SGD epilogue of one tile of any chunk, from local memory (G already stored).
+__device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTile& d,
+                                            int lane_id) {
+  const size_t mine = (size_t)r * kp.T + d.t;
+  const float* pg = kp.a[mine] + d.e;
+  float* pw = kp.b[mine] + d.e;
+  float* pd = kp.c[mine] + d.e;
+  const bool vec = d.full && ((((uintptr_t)pg | (uintptr_t)pw | (uintptr_t)pd) & 15) == 0);
+  if (vec) {
+    constexpr int U = 2;
+    for (int s0 = lane_id; s0 < d.n; s0 += 32 * U) {
+      float4 g[U], w[U], dw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + 32 * u;
+        if (s < d.n) {
+          g[u] = ld16(pg + 4 * s);
+          w[u] = ld16(pw + 4 * s);
+          dw[u] = ld16(pd + 4 * s);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + 32 * u;
+        if (s >= d.n) continue;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) sgd1(kp, lane_of(g[u], l), lane(w[u], l), lane(dw[u], l));
+        st16(pw + 4 * s, w[u]);
+        st16(pd + 4 * s, dw[u]);
+      }
+    }
+  } else {
+    const int64_t j0 = d.e < 0 ? -d.e : 0;
+    const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
+    for (int64_t j = j0 + lane_id; j < j1; j += 32) {
+      float w = ld4(pw + j), dw = ld4(pd + j);
+      sgd1(kp, ld4(pg + j), w, dw);
+      st4(pw + j, w);
+      st4(pd + j, dw);
+    }
+  }
+}
+
+// Lane 0: wait until owner q's CTA (this CTA's index) has published `rounds` rounds.
+__device__ __forceinline__ bool nv_wait(const KParams& kp, int r, int q, int rounds) {
+  const uint32_t* f = kp.flags[r] + flag_index(BAR_PROG, q, blockIdx.x);
+  const uint32_t want = nv_flag_value(rounds);
+  if ((int32_t)(ld_acquire_sys(f) - want) >= 0) return true;
+  const unsigned long long t0 = globaltimer();
+  while ((int32_t)(ld_acquire_sys(f) - want) < 0)
+    if (globaltimer() - t0 > kp.timeout_ns) {
+      atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
+      return false;
+    }
+  return true;
+}
+
+template <int OP, int P>
+__global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
+  constexpr int NW = nvls_reduce_warps(OP);  // switch-reduction warps; warp NW signals
+  constexpr int NE = kNvlsWarps - NW - 1;    // SGD epilogue warps
+  const int r = kp.rank0 + (int)blockIdx.y;
+  if (r == kp.absent_rank) return;
+  call_begin(kp, r);
+  const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  const int b = (int)blockIdx.x, G = (int)gridDim.x;
+  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;  // every rank's data is in place
+  int cnt, tpr;
+  nv_counts(kp, r, NW, cnt, tpr);
+  const int nr = (cnt + tpr - 1) / tpr;
+  bool ok = true;
+  if (warp < NW) {
+    for (int j = 0; j < nr; ++j) {
+      for (int k = j * tpr + warp; k < min(cnt, (j + 1) * tpr); k += NW)
+        nv_reduce_tile<OP>(kp, nv_tile(kp, kp.tile2_off[r] + b + G * k), lane_id);
+      __syncwarp();
+      // every reduction warp syncs too: a warp must not arrive twice at one barrier phase
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
+    }
+  } else if (warp == NW) {
+    for (int j = 0; j < nr; ++j) {
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
+      if (lane_id == 0) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int q = 0; q < P; ++q)
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(
+                           kp.flags[q] + flag_index(BAR_PROG, r, b)),
+                       "r"(nv_flag_value(j + 1))
+                       : "memory");
+      }
+      __syncwarp();
+    }
+    if constexpr (OP != OP_SGD) {
+      // every owner's stores have landed here before the call completes
+      if (lane_id < P) {
+        int cq, tq;
+        nv_counts(kp, lane_id, NW, cq, tq);
+        if (cq > 0) ok = nv_wait(kp, r, lane_id, (cq + tq - 1) / tq);
+      }
+      ok = __all_sync(0xffffffffu, ok);
+    }
+  } else if constexpr (OP == OP_SGD) {
+    const int ew = warp - NW - 1;
+#pragma unroll 1
+    for (int jq = 0; jq < P && ok; ++jq) {
+      const int q = (r + jq) % P;  // own chunk first: its rounds are published first
+      int cq, tq;
+      nv_counts(kp, q, NW, cq, tq);
+      const int nq = (cq + tq - 1) / tq;
+      for (int j = 0; j < nq && ok; ++j) {
+        if (lane_id == 0) ok = nv_wait(kp, r, q, j + 1);
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        __syncwarp();
+        for (int k = j * tq + ew; k < min(cq, (j + 1) * tq) && ok; k += NE)
+          nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id);
+      }
+    }
+  }
+  if (!__syncthreads_and(ok)) return;
+  call_end(kp, r);
+}
+
 template <int OP>
 const void* kernel_ptr(int algo, int p) {
   if (algo == ALGO_LOCAL) return (const void*)k_local_tma<OP>;
 #define TC_CASE(PP)                                                                          \
   case PP:                                                                                   \
     if constexpr (OP != OP_EASGD)                                                            \
-      if (algo == ALGO_NVLS) return (const void*)k_nvls<OP, PP, 2>;                          \
+      if (algo == ALGO_NVLS) return (const void*)k_nvls<OP, PP>;                             \
     if (algo == ALGO_NVLS) return nullptr;                                                   \
     if (algo == ALGO_TWOSHOT_TMA) return (const void*)k_twoshot_tma<OP, PP>;                 \
     if (algo == ALGO_TWOSHOT_BAL) return (const void*)k_twoshot_bal<OP, PP>;                 \

@@ -445,11 +445,11 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (occ < 1) return TC_ERR_CUDA;
   int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
   if (cap < 1) cap = 1;
-  const bool twoshot = algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH || algo == ALGO_NVLS;
+  const bool twoshot = algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH;
   int64_t work_slots = twoshot ? (Mdev + p - 1) / p : Mdev;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
-  if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL) {
+  if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL || algo == ALGO_NVLS) {
     // bytes in flight come from the stage ring, not from threads: one CTA per SM at most
     const int tiles_r = ga->tile2_off[1] - ga->tile2_off[0];
     ctas = tune_ctas > 0 ? tune_ctas : c.num_sms;
@@ -463,10 +463,6 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     kp.ntiles = ga->ntiles;
   } else if (twoshot && tune_ctas > 0) {
     ctas = tune_ctas;
-  } else if (algo == ALGO_NVLS && op == OP_ALLREDUCE) {
-    // switch reductions saturate with ~half the SMs (p = 4 allreduce: 74 CTAs 285 us,
-    // 148 x 512 299, 296 x 512 307); the SGD epilogue pass wants the full grid (392 vs 470 us)
-    ctas = (int)std::min<int64_t>(want, c.num_sms / 2);
   } else {
     ctas = (int)std::min<int64_t>(
         want, (int64_t)c.num_sms * ((algo == ALGO_ONESHOT || algo == ALGO_LL) ? 1 : occ));

@@ -263,7 +263,7 @@ def cpu_baseline_sgd(numels, p, budget_s=20.0):
 
 
 # ------------------------------------------------------------------ the reference arm
-def run_reference(args):
+def run_reference(args, jsonout):
     """The tier's reference arm: the CPU oracle as it stands, on our arm's workload (the whole
     p-rank fused step on the full group every step), on all host cores of rank 0."""
     rank, world, _ = dist_env()
@@ -296,7 +296,7 @@ def run_reference(args):
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": o.cores, "kind": "oracle",
                          "sample": desc},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }), file=jsonout, flush=True)
 
 
 # ------------------------------------------------------------------ the product arm
@@ -373,7 +373,17 @@ def nccl_allreduce_us(flat, stream, warmup, K, world, group=None):
     return max_over_ranks(e0.elapsed_time(e1) / K, world) * 1e3
 
 
+def claim_stdout():
+    """Only the JSON line may reach stdout: the process's fd 1 is pointed at stderr (NCCL prints
+    its version banner there) and the returned file writes to the original stdout."""
+    sys.stdout.flush()
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    return out
+
+
 def main():
+    jsonout = claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -394,7 +404,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args, jsonout)
 
     import torch
     rank, world, local = dist_env()
@@ -736,7 +746,7 @@ def main():
         grp.destroy()
     comm.destroy()
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=jsonout, flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

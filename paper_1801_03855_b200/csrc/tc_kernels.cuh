@@ -1700,13 +1700,20 @@ __device__ __forceinline__ NvTile nv_tile(const KParams& kp, int gi) {
   return d;
 }
 
-// Tiles of owner q's chunk held by this CTA, and the tiles per round.
+// Tiles of owner q's chunk held by this CTA, and the tiles per published round: one tile per
+// reduction warp for the SGD step (its epilogue follows the rounds), all of them at once for the
+// plain allreduce (nothing to overlap: only the end is awaited).
+template <int OP>
 __device__ __forceinline__ void nv_counts(const KParams& kp, int q, int nw, int& cnt, int& tpr) {
   const int n = kp.tile2_off[q + 1] - kp.tile2_off[q];
   const int b = (int)blockIdx.x, G = (int)gridDim.x;
   cnt = n > b ? (n - b + G - 1) / G : 0;
-  const int m = (cnt + 255 * nw - 1) / (255 * nw);
-  tpr = nw * (m > 0 ? m : 1);
+  if constexpr (OP != OP_SGD) {
+    tpr = cnt > 0 ? cnt : 1;
+  } else {
+    const int m = (cnt + 255 * nw - 1) / (255 * nw);
+    tpr = nw * (m > 0 ? m : 1);
+  }
 }
 __device__ __forceinline__ uint32_t nv_flag_value(int rounds) {
   return (ep() << 8) | (uint32_t)rounds;
@@ -1784,18 +1791,25 @@ __device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTi
   }
 }
 
-// Lane 0: wait until owner q's CTA (this CTA's index) has published `rounds` rounds.
+// One lane: wait until owner q's CTA (this CTA's index) has published `rounds` rounds.  Polls
+// with relaxed loads and a short sleep (acquire loads in a tight loop from several warps slow the
+// SM's other memory traffic), then one acquire load orders the data reads after the flag.
 __device__ __forceinline__ bool nv_wait(const KParams& kp, int r, int q, int rounds) {
   const uint32_t* f = kp.flags[r] + flag_index(BAR_PROG, q, blockIdx.x);
   const uint32_t want = nv_flag_value(rounds);
   if ((int32_t)(ld_acquire_sys(f) - want) >= 0) return true;
   const unsigned long long t0 = globaltimer();
-  while ((int32_t)(ld_acquire_sys(f) - want) < 0)
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if ((int32_t)(v - want) >= 0) break;
+    __nanosleep(128);
     if (globaltimer() - t0 > kp.timeout_ns) {
       atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
       return false;
     }
-  return true;
+  }
+  return (int32_t)(ld_acquire_sys(f) - want) >= 0;
 }
 
 template <int OP, int P>
@@ -1809,7 +1823,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
   const int b = (int)blockIdx.x, G = (int)gridDim.x;
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;  // every rank's data is in place
   int cnt, tpr;
-  nv_counts(kp, r, NW, cnt, tpr);
+  nv_counts<OP>(kp, r, NW, cnt, tpr);
   const int nr = (cnt + tpr - 1) / tpr;
   bool ok = true;
   if (warp < NW) {
@@ -1837,7 +1851,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
       // every owner's stores have landed here before the call completes
       if (lane_id < P) {
         int cq, tq;
-        nv_counts(kp, lane_id, NW, cq, tq);
+        nv_counts<OP>(kp, lane_id, NW, cq, tq);
         if (cq > 0) ok = nv_wait(kp, r, lane_id, (cq + tq - 1) / tq);
       }
       ok = __all_sync(0xffffffffu, ok);
@@ -1848,7 +1862,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
     for (int jq = 0; jq < P && ok; ++jq) {
       const int q = (r + jq) % P;  // own chunk first: its rounds are published first
       int cq, tq;
-      nv_counts(kp, q, NW, cq, tq);
+      nv_counts<OP>(kp, q, NW, cq, tq);
       const int nq = (cq + tq - 1) / tq;
       for (int j = 0; j < nq && ok; ++j) {
         if (lane_id == 0) ok = nv_wait(kp, r, q, j + 1);

@@ -86,8 +86,8 @@ __device__ __forceinline__ float& lane(float4& v, int i) { return (&v.x)[i]; }
 __device__ __forceinline__ float lane_of(const float4& v, int i) { return (&v.x)[i]; }
 
 // Phase timestamp (diagnostics only; kp.prof == nullptr in production).
-__device__ __forceinline__ void stamp(const KParams& kp, int i) {
-  if (kp.prof != nullptr && threadIdx.x == 0)
+__device__ __forceinline__ void stamp(const KParams& kp, int i, int tid = 0) {
+  if (kp.prof != nullptr && (int)threadIdx.x == tid)
     kp.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = globaltimer();
 }
 
@@ -1680,7 +1680,18 @@ __device__ __forceinline__ void mm_st4(float* p, float v) {
 }
 
 constexpr int kNvlsWarps = kNvlsThreads / 32;
-__host__ __device__ constexpr int nvls_reduce_warps(int op) { return op == OP_ALLREDUCE ? 12 : 6; }
+#ifndef TC_NV_RW_AR
+#define TC_NV_RW_AR 12  // switch-reduction warps per CTA, plain allreduce
+#endif
+#ifndef TC_NV_RW_SGD
+#define TC_NV_RW_SGD 6  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
+#endif
+#ifndef TC_NV_ROUND
+#define TC_NV_ROUND 1   // fused SGD: tiles per reduction warp per published round
+#endif
+__host__ __device__ constexpr int nvls_reduce_warps(int op) {
+  return op == OP_ALLREDUCE ? TC_NV_RW_AR : TC_NV_RW_SGD;
+}
 
 // A tile of owner q's chunk as seen by this rank: element offset e of its first slot inside
 // tensor t (negative for a shifted head), slot count n, vector path when the tile is whole
@@ -1712,7 +1723,7 @@ __device__ __forceinline__ void nv_counts(const KParams& kp, int q, int nw, int&
     tpr = cnt > 0 ? cnt : 1;
   } else {
     const int m = (cnt + 255 * nw - 1) / (255 * nw);
-    tpr = nw * (m > 0 ? m : 1);
+    tpr = nw * (m > TC_NV_ROUND ? m : TC_NV_ROUND);
   }
 }
 __device__ __forceinline__ uint32_t nv_flag_value(int rounds) {
@@ -1821,7 +1832,9 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
   call_begin(kp, r);
   const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   const int b = (int)blockIdx.x, G = (int)gridDim.x;
+  stamp(kp, 0);
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;  // every rank's data is in place
+  stamp(kp, 1);
   int cnt, tpr;
   nv_counts<OP>(kp, r, NW, cnt, tpr);
   const int nr = (cnt + tpr - 1) / tpr;
@@ -1834,6 +1847,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
       // every reduction warp syncs too: a warp must not arrive twice at one barrier phase
       asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
     }
+    stamp(kp, 2);  // (diagnostics) reduction warps done
   } else if (warp == NW) {
     for (int j = 0; j < nr; ++j) {
       asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
@@ -1847,6 +1861,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
       }
       __syncwarp();
     }
+    stamp(kp, 3, 32 * NW);  // (diagnostics) every round published
     if constexpr (OP != OP_SGD) {
       // every owner's stores have landed here before the call completes
       if (lane_id < P) {
@@ -1855,6 +1870,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
         if (cq > 0) ok = nv_wait(kp, r, lane_id, (cq + tq - 1) / tq);
       }
       ok = __all_sync(0xffffffffu, ok);
+      stamp(kp, 4, 32 * NW);  // (diagnostics) every owner's last round seen
     }
   } else if constexpr (OP == OP_SGD) {
     const int ew = warp - NW - 1;
@@ -1872,9 +1888,11 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
           nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id);
       }
     }
+    stamp(kp, 4, 32 * (kNvlsWarps - 1));  // (diagnostics) last epilogue warp done
   }
   if (!__syncthreads_and(ok)) return;
   call_end(kp, r);
+  stamp(kp, 5);
 }
 
 template <int OP>

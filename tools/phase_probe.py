@@ -52,7 +52,8 @@ def main():
     comm.set_algorithm(a.algo)
     prof = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
     G, Wg, D = tc.Group(comm, g), tc.Group(comm, w), tc.Group(comm, dw)
-    names = ["entry", "RS", "mid", "AG", "exit"]
+    names = (["entry", "reduce", "signal", "epilogue/wait", "end"] if a.algo == 4 else
+             ["entry", "RS", "mid", "AG", "exit"])
     for op in ("allreduce", "sgd"):
         comm.set_profile_buffer(None)
         for i in range(a.iters):

@@ -1759,9 +1759,10 @@ __device__ __forceinline__ void nv_reduce_tile(const KParams& kp, const NvTile& 
   }
 }
 
-// Whole warp: the SGD epilogue of one tile of any chunk, from local memory (G already stored).
-__device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTile& d,
-                                            int lane_id) {
+// Threads ct of nct (the epilogue warps together): the SGD epilogue of one tile of any chunk,
+// from local memory (G already stored by its owner).
+__device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTile& d, int ct,
+                                            int nct) {
   const size_t mine = (size_t)r * kp.T + d.t;
   const float* pg = kp.a[mine] + d.e;
   float* pw = kp.b[mine] + d.e;
@@ -1769,11 +1770,11 @@ __device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTi
   const bool vec = d.full && ((((uintptr_t)pg | (uintptr_t)pw | (uintptr_t)pd) & 15) == 0);
   if (vec) {
     constexpr int U = 2;
-    for (int s0 = lane_id; s0 < d.n; s0 += 32 * U) {
+    for (int s0 = ct; s0 < d.n; s0 += nct * U) {
       float4 g[U], w[U], dw[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int s = s0 + 32 * u;
+        const int s = s0 + nct * u;
         if (s < d.n) {
           g[u] = ld16(pg + 4 * s);
           w[u] = ld16(pw + 4 * s);
@@ -1782,7 +1783,7 @@ __device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTi
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int s = s0 + 32 * u;
+        const int s = s0 + nct * u;
         if (s >= d.n) continue;
 #pragma unroll
         for (int l = 0; l < 4; ++l) sgd1(kp, lane_of(g[u], l), lane(w[u], l), lane(dw[u], l));
@@ -1793,7 +1794,7 @@ __device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTi
   } else {
     const int64_t j0 = d.e < 0 ? -d.e : 0;
     const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
-    for (int64_t j = j0 + lane_id; j < j1; j += 32) {
+    for (int64_t j = j0 + ct; j < j1; j += nct) {
       float w = ld4(pw + j), dw = ld4(pd + j);
       sgd1(kp, ld4(pg + j), w, dw);
       st4(pw + j, w);
@@ -1884,8 +1885,9 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
         if (lane_id == 0) ok = nv_wait(kp, r, q, j + 1);
         ok = __shfl_sync(0xffffffffu, ok, 0);
         __syncwarp();
-        for (int k = j * tq + ew; k < min(cq, (j + 1) * tq) && ok; k += NE)
-          nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id);
+        // every epilogue warp takes a share of every tile of the round
+        for (int k = j * tq; k < min(cq, (j + 1) * tq) && ok; ++k)
+          nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id + 32 * ew, 32 * NE);
       }
     }
     stamp(kp, 4, 32 * (kNvlsWarps - 1));  // (diagnostics) last epilogue warp done

@@ -1686,6 +1686,9 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #ifndef TC_NV_RW_SGD
 #define TC_NV_RW_SGD 6  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
 #endif
+#ifndef TC_NV_EPI_U
+#define TC_NV_EPI_U 4   // fused SGD epilogue: 16-B slots per thread in flight
+#endif
 #ifndef TC_NV_ROUND
 #define TC_NV_ROUND 1   // fused SGD: tiles per reduction warp per published round
 #endif
@@ -1769,7 +1772,7 @@ __device__ __forceinline__ void nv_sgd_tile(const KParams& kp, int r, const NvTi
   float* pd = kp.c[mine] + d.e;
   const bool vec = d.full && ((((uintptr_t)pg | (uintptr_t)pw | (uintptr_t)pd) & 15) == 0);
   if (vec) {
-    constexpr int U = 2;
+    constexpr int U = TC_NV_EPI_U;  // slots per thread in flight (3 loads each)
     for (int s0 = ct; s0 < d.n; s0 += nct * U) {
       float4 g[U], w[U], dw[U];
 #pragma unroll

@@ -1686,6 +1686,9 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #ifndef TC_NV_RW_SGD
 #define TC_NV_RW_SGD 6  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
 #endif
+#ifndef TC_NV_RED_U_SGD
+#define TC_NV_RED_U_SGD 4  // fused SGD: switch reductions in flight per lane
+#endif
 #ifndef TC_NV_EPI_U
 #define TC_NV_EPI_U 4   // fused SGD epilogue: 16-B slots per thread in flight
 #endif
@@ -1742,7 +1745,7 @@ __device__ __forceinline__ void nv_reduce_tile(const KParams& kp, const NvTile& 
     return OP == OP_ALLREDUCE ? __double2float_rn(__dmul_rn((double)v, (double)kp.scale)) : v;
   };
   if (vec) {
-    constexpr int U = 4;
+    constexpr int U = OP == OP_SGD ? TC_NV_RED_U_SGD : 4;  // switch reductions in flight per lane
     for (int s0 = lane_id; s0 < d.n; s0 += 32 * U) {
       float4 v[U];
 #pragma unroll
@@ -1892,6 +1895,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
         for (int k = j * tq; k < min(cq, (j + 1) * tq) && ok; ++k)
           nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id + 32 * ew, 32 * NE);
       }
+      if (jq < 2) stamp(kp, 6 + jq, 32 * (kNvlsWarps - 1));  // (diagnostics) chunks r, r+1 done
     }
     stamp(kp, 4, 32 * (kNvlsWarps - 1));  // (diagnostics) last epilogue warp done
   }

@@ -1686,6 +1686,9 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #ifndef TC_NV_RW_SGD
 #define TC_NV_RW_SGD 6  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
 #endif
+#ifndef TC_NV_FENCE
+#define TC_NV_FENCE 0   // 0: the signal warp fences; 1: every reduction warp fences its own
+#endif                  // stores (2: no fence -- timing experiments only, not ordered)
 #ifndef TC_NV_RED_U_SGD
 #define TC_NV_RED_U_SGD 4  // fused SGD: switch reductions in flight per lane
 #endif
@@ -1851,6 +1854,10 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
       for (int k = j * tpr + warp; k < min(cnt, (j + 1) * tpr); k += NW)
         nv_reduce_tile<OP>(kp, nv_tile(kp, kp.tile2_off[r] + b + G * k), lane_id);
       __syncwarp();
+#if TC_NV_FENCE == 1
+      // each reduction warp makes its own stores visible system-wide before the round closes
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
       // every reduction warp syncs too: a warp must not arrive twice at one barrier phase
       asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
     }
@@ -1859,12 +1866,19 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
     for (int j = 0; j < nr; ++j) {
       asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
       if (lane_id == 0) {
+#if TC_NV_FENCE == 0
         asm volatile("fence.acq_rel.sys;" ::: "memory");
-        for (int q = 0; q < P; ++q)
+#endif
+        for (int q = 0; q < P; ++q) {
+#if TC_NV_FENCE == 1
+          st_release_sys(kp.flags[q] + flag_index(BAR_PROG, r, b), nv_flag_value(j + 1));
+#else
           asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(
                            kp.flags[q] + flag_index(BAR_PROG, r, b)),
                        "r"(nv_flag_value(j + 1))
                        : "memory");
+#endif
+        }
       }
       __syncwarp();
     }

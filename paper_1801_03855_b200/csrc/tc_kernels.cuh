@@ -1895,21 +1895,33 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
     }
   } else if constexpr (OP == OP_SGD) {
     const int ew = warp - NW - 1;
-#pragma unroll 1
-    for (int jq = 0; jq < P && ok; ++jq) {
-      const int q = (r + jq) % P;  // own chunk first: its rounds are published first
+    // round by round over every owner (round j of every chunk before round j + 1 of any): the
+    // owners publish their rounds at about the same pace, so only the last round's epilogue
+    // is left when the switch work ends
+    int nmax = 0;
+    for (int q = 0; q < P; ++q) {
       int cq, tq;
       nv_counts<OP>(kp, q, NW, cq, tq);
-      const int nq = (cq + tq - 1) / tq;
-      for (int j = 0; j < nq && ok; ++j) {
+      nmax = max(nmax, (cq + tq - 1) / tq);
+    }
+#pragma unroll 1
+    for (int j = 0; j < nmax && ok; ++j) {
+#pragma unroll 1
+      for (int jq = 0; jq < P && ok; ++jq) {
+        const int q = (r + jq) % P;  // own chunk first: its round is published first
+        int cq, tq;
+        nv_counts<OP>(kp, q, NW, cq, tq);
+        if (j * tq >= cq) continue;
         if (lane_id == 0) ok = nv_wait(kp, r, q, j + 1);
         ok = __shfl_sync(0xffffffffu, ok, 0);
         __syncwarp();
         // every epilogue warp takes a share of every tile of the round
         for (int k = j * tq; k < min(cq, (j + 1) * tq) && ok; ++k)
-          nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id + 32 * ew, 32 * NE);
+          nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id + 32 * ew,
+                      32 * NE);
       }
-      if (jq < 2) stamp(kp, 6 + jq, 32 * (kNvlsWarps - 1));  // (diagnostics) chunks r, r+1 done
+      if (j == 0) stamp(kp, 6, 32 * (kNvlsWarps - 1));  // (diagnostics) first round done
+      if (j == 1) stamp(kp, 7, 32 * (kNvlsWarps - 1));  // (diagnostics) second round done
     }
     stamp(kp, 4, 32 * (kNvlsWarps - 1));  // (diagnostics) last epilogue warp done
   }

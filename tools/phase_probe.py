@@ -70,8 +70,8 @@ def main():
         span = (t[:, 5].max() - t[:, 0].min()) / 1e3
         line = " ".join(f"{n}={np.median(d[:, i]):7.1f}/{d[:, i].max():7.1f}" for i, n in enumerate(names))
         if a.algo == 4 and op == "sgd":  # NVLS: epilogue of the own chunk / the next one done
-            line += (f" | own chunk epilogue done at {np.median(t[:, 6] - t[:, 1]) / 1e3:7.1f}"
-                     f", next chunk at {np.median(t[:, 7] - t[:, 1]) / 1e3:7.1f} (from entry)")
+            line += (f" | epilogue of round 0 done at {np.median(t[:, 6] - t[:, 1]) / 1e3:7.1f}"
+                     f", round 1 at {np.median(t[:, 7] - t[:, 1]) / 1e3:7.1f} (from entry)")
         if a.algo == 6:  # TMA two-shot: producer waiting for free stages / consumers for data
             wf = t[:, 7] & ((1 << 40) - 1)
             smid = t[:, 7] >> 40

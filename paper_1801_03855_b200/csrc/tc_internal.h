@@ -85,6 +85,10 @@ constexpr int t2_smem(int op, int p) {
 }
 
 constexpr int kNvlsThreads = 512;              // NVLS: 16 warps (reduction / signal / epilogue)
+#ifndef TC_NV_SLOTS
+#define TC_NV_SLOTS 128
+#endif
+constexpr int kNvSlots = TC_NV_SLOTS;           // NVLS tile: <= 128 slots = 2 KiB per operand
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_PROG = 2 };  // PROG: NVLS round progress
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4, OP_EASYNC = 5 };
 enum Algo {
@@ -255,6 +259,8 @@ struct Group {
   int ntiles = 0;
   int4* d_tiles2 = nullptr;      // p >= 2: owner-chunk tiles of the TMA two-shot
   std::vector<int> tile2_off;    // [p + 1]
+  int4* d_tiles_nv = nullptr;    // NVLS-eligible groups: owner-chunk tiles of <= kNvSlots slots
+  std::vector<int> tile_nv_off;  // [p + 1]
   std::vector<void*> sym_bases;  // symmetric allocations (this rank's base) the group uses
   int num_ctas = 0;              // per-group CTA budget (0 = the comm's tuning)
 };

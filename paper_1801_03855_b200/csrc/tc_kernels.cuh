@@ -1904,6 +1904,7 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
       nv_counts<OP>(kp, q, NW, cq, tq);
       nmax = max(nmax, (cq + tq - 1) / tq);
     }
+    int item = 0;  // running index over (round, owner, tile): epilogue warp ew takes ew mod NE
 #pragma unroll 1
     for (int j = 0; j < nmax && ok; ++j) {
 #pragma unroll 1
@@ -1911,14 +1912,16 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
         const int q = (r + jq) % P;  // own chunk first: its round is published first
         int cq, tq;
         nv_counts<OP>(kp, q, NW, cq, tq);
-        if (j * tq >= cq) continue;
+        const int k0 = j * tq, k1 = min(cq, (j + 1) * tq);
+        if (k0 >= k1) continue;
+        int k = k0 + ((ew - item) % NE + NE) % NE;  // this warp's first item of the round
+        item += k1 - k0;
+        if (k >= k1) continue;
         if (lane_id == 0) ok = nv_wait(kp, r, q, j + 1);
         ok = __shfl_sync(0xffffffffu, ok, 0);
         __syncwarp();
-        // every epilogue warp takes a share of every tile of the round
-        for (int k = j * tq; k < min(cq, (j + 1) * tq) && ok; ++k)
-          nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id + 32 * ew,
-                      32 * NE);
+        for (; k < k1 && ok; k += NE)
+          nv_sgd_tile(kp, r, nv_tile(kp, kp.tile2_off[q] + b + G * k), lane_id, 32);
       }
       if (j == 0) stamp(kp, 6, 32 * (kNvlsWarps - 1));  // (diagnostics) first round done
       if (j == 1) stamp(kp, 7, 32 * (kNvlsWarps - 1));  // (diagnostics) second round done

@@ -155,6 +155,8 @@ void free_group_device(Group& g) {
   g.ntiles = 0;
   cudaFree(g.d_tiles2);
   g.d_tiles2 = nullptr;
+  cudaFree(g.d_tiles_nv);
+  g.d_tiles_nv = nullptr;
   g.tile2_off.clear();
   g.d_ptrs = nullptr;
   g.d_prefix = nullptr;
@@ -235,36 +237,49 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
   if (g.comm->nranks > 1) {
     // TMA two-shot: each owner chunk [M q / p, M (q+1) / p) of the device grid cut into tiles
     // of <= kT2Slots slots inside one tensor.  A shifted tensor's partial first slot and a
-    // partial last slot are one-slot tiles of their own (element path in the kernel).
+    // partial last slot are one-slot tiles of their own (element path in the kernel).  NVLS-
+    // eligible groups get a second table with smaller tiles (kNvSlots: finer published rounds).
     const int p = g.comm->nranks;
-    std::vector<int4> tiles;
-    g.tile2_off.assign((size_t)p + 1, 0);
-    int t = 0;
-    for (int q = 0; q < p; ++q) {
-      g.tile2_off[(size_t)q] = (int)tiles.size();
-      const int64_t lo = g.M * q / p, hi = g.M * (q + 1) / p;
-      while (t < pl.T && g.dev_prefix[(size_t)t + 1] <= lo) ++t;
-      for (int u = t; u < pl.T && g.dev_prefix[(size_t)u] < hi; ++u) {
-        const int64_t pre = g.dev_prefix[(size_t)u], end = g.dev_prefix[(size_t)u + 1];
-        int64_t a = std::max(lo, pre);
-        const int64_t b = std::min(hi, end);
-        if (a >= b) continue;
-        const int64_t m = g.shift[(size_t)u], n = pl.numel[(size_t)u];
-        const int64_t first_full = pre + (m ? 1 : 0);
-        const int64_t full_end = end - (((n + m) & 3) ? 1 : 0);
-        if (a < first_full) tiles.push_back(make_int4(u, (int)a++, 1, 0));
-        const int64_t vend = std::min(b, full_end);
-        for (int64_t x = a; x < vend; x += t2_slots(p))
-          tiles.push_back(make_int4(u, (int)x, (int)std::min<int64_t>(t2_slots(p), vend - x), 0));
-        const int64_t rest = std::max(a, vend);
-        if (b > rest) tiles.push_back(make_int4(u, (int)rest, (int)(b - rest), 0));
+    auto build = [&](int64_t cap, std::vector<int>& off) {
+      std::vector<int4> tiles;
+      off.assign((size_t)p + 1, 0);
+      int t = 0;
+      for (int q = 0; q < p; ++q) {
+        off[(size_t)q] = (int)tiles.size();
+        const int64_t lo = g.M * q / p, hi = g.M * (q + 1) / p;
+        while (t < pl.T && g.dev_prefix[(size_t)t + 1] <= lo) ++t;
+        for (int u = t; u < pl.T && g.dev_prefix[(size_t)u] < hi; ++u) {
+          const int64_t pre = g.dev_prefix[(size_t)u], end = g.dev_prefix[(size_t)u + 1];
+          int64_t a = std::max(lo, pre);
+          const int64_t b = std::min(hi, end);
+          if (a >= b) continue;
+          const int64_t m = g.shift[(size_t)u], n = pl.numel[(size_t)u];
+          const int64_t first_full = pre + (m ? 1 : 0);
+          const int64_t full_end = end - (((n + m) & 3) ? 1 : 0);
+          if (a < first_full) tiles.push_back(make_int4(u, (int)a++, 1, 0));
+          const int64_t vend = std::min(b, full_end);
+          for (int64_t x = a; x < vend; x += cap)
+            tiles.push_back(make_int4(u, (int)x, (int)std::min<int64_t>(cap, vend - x), 0));
+          const int64_t rest = std::max(a, vend);
+          if (b > rest) tiles.push_back(make_int4(u, (int)rest, (int)(b - rest), 0));
+        }
       }
-    }
-    g.tile2_off[(size_t)p] = (int)tiles.size();
+      off[(size_t)p] = (int)tiles.size();
+      return tiles;
+    };
+    std::vector<int4> tiles = build(t2_slots(p), g.tile2_off);
     if (!tiles.empty()) {
       TC_CUDA(cudaMalloc((void**)&g.d_tiles2, sizeof(int4) * tiles.size()));
       TC_CUDA(cudaMemcpy(g.d_tiles2, tiles.data(), sizeof(int4) * tiles.size(),
                          cudaMemcpyHostToDevice));
+    }
+    if (!g.h_mc.empty()) {
+      std::vector<int4> nt = build(kNvSlots, g.tile_nv_off);
+      if (!nt.empty()) {
+        TC_CUDA(cudaMalloc((void**)&g.d_tiles_nv, sizeof(int4) * nt.size()));
+        TC_CUDA(cudaMemcpy(g.d_tiles_nv, nt.data(), sizeof(int4) * nt.size(),
+                           cudaMemcpyHostToDevice));
+      }
     }
   }
   if (!g.h_mc.empty()) {
@@ -451,11 +466,13 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   int ctas;
   if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL || algo == ALGO_NVLS) {
     // bytes in flight come from the stage ring, not from threads: one CTA per SM at most
-    const int tiles_r = ga->tile2_off[1] - ga->tile2_off[0];
+    // (NVLS walks its own table of smaller tiles)
+    const std::vector<int>& off = algo == ALGO_NVLS ? ga->tile_nv_off : ga->tile2_off;
+    const int tiles_r = off[1] - off[0];
     ctas = tune_ctas > 0 ? tune_ctas : c.num_sms;
     ctas = std::max(1, std::min(ctas, std::max(tiles_r, 1)));
-    kp.tiles2 = ga->d_tiles2;
-    for (int q = 0; q <= p; ++q) kp.tile2_off[q] = ga->tile2_off[(size_t)q];
+    kp.tiles2 = algo == ALGO_NVLS ? ga->d_tiles_nv : ga->d_tiles2;
+    for (int q = 0; q <= p; ++q) kp.tile2_off[q] = off[(size_t)q];
   } else if (algo == ALGO_LOCAL) {  // TMA stream
     ctas = std::min(ga->ntiles, tune_ctas > 0 ? std::min(tune_ctas, c.num_sms * occ)
                                                 : c.num_sms * occ);

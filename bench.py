@@ -397,8 +397,9 @@ def main():
                     help="only the step (and e2e): skip allreduce/broadcast/NCCL/EASGD/config-4")
     ap.add_argument("--algo", type=int, default=0,
                     help="0 auto, 1 two-shot pull, 3 two-shot push, 4 NVLS, 6 TMA, 7 balanced")
-    ap.add_argument("--switch", action="store_true",
-                    help="let the automatic choice use NVLS (tc_comm_set_switch_reduction)")
+    ap.add_argument("--switch", default="auto", choices=["auto", "on", "off"],
+                    help="let the automatic choice use NVLS (tc_comm_set_switch_reduction): "
+                         "auto = from N = 5, where it moves fewer bytes than the two-shot")
     ap.add_argument("--no-sym", action="store_true",
                     help="keep gradients in torch memory (no NVLS) instead of tc_mem_alloc")
     args = ap.parse_args()
@@ -436,7 +437,8 @@ def main():
 
     comm = tc.Comm.single(local) if p == 1 else tc.Comm.from_process_group(device=local)
     comm.set_algorithm(args.algo)
-    if args.switch:
+    switch = args.switch == "on" or (args.switch == "auto" and p >= 5)
+    if switch:
         comm.set_switch_reduction(True)
     sym = p > 1 and not args.no_sym
     if sym:
@@ -735,7 +737,7 @@ def main():
         "config": workload_config(args.config, numels, p),
         "launch": {"algo": algo, "ctas": ctas, "threads": threads,
                    "grad_memory": "tc_mem_alloc (symmetric, multicast)" if sym else "torch",
-                   "switch_reduction_allowed": bool(args.switch)},
+                   "switch_reduction_allowed": switch},
         "whole_job_gbs": p * S / t_s / 1e9, "busbw_gbs": value if p > 1 else 0.0,
         "algbw_gbs": algbw, "t_us": t_ms * 1e3,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

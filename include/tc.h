@@ -162,8 +162,9 @@ TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 /* Whether the AUTOMATIC choice may use the NVSwitch reduction (algorithm 4) for groups in
  * tc_mem_alloc memory (must be identical on all ranks).  0 (default): never -- every automatic
  * result is bit-identical to the float64 rank-order oracle.  1: allowed where it moves fewer
- * bytes per GPU than the two-shot ((1 + 1/p) S against 2(p-1)/p S, p >= 6 with the p = 4
- * measured rates) -- results then follow algorithm 4's tolerance contract.
+ * bytes per GPU than the two-shot ((1 + 1/p) S against 2(p-1)/p S, with the p = 4
+ * measured rates: from p = 5 for tc_allreduce and tc_sgd_step) -- results then
+ * follow algorithm 4's tolerance contract.
  * Errors: TC_ERR_INVALID_ARG (allow not 0 or 1). */
 TC_API tc_status tc_comm_set_switch_reduction(tc_comm* comm, int allow);
 

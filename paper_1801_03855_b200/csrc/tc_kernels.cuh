@@ -1684,7 +1684,7 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #define TC_NV_RW_AR 12  // switch-reduction warps per CTA, plain allreduce
 #endif
 #ifndef TC_NV_RW_SGD
-#define TC_NV_RW_SGD 6  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
+#define TC_NV_RW_SGD 4  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
 #endif
 #ifndef TC_NV_FENCE
 #define TC_NV_FENCE 0   // 0: the signal warp fences; 1: every reduction warp fences its own

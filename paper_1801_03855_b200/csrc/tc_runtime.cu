@@ -423,9 +423,12 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     if (lim > (int64_t)kStageCapacity) lim = (int64_t)kStageCapacity;
     // Automatic choice (measured on B200, config-5 sweep and ResNet-50 group):
     // TMA-staged two-shot (p = 4: 16/64/256 MiB in 58-67/176-184/635-650 us; LDG pull
-    // 72/189/679, pushed 95/210/737, NCCL 70/186/685); p >= 6 -> NVLS for the allreduce of a
-    // multicast-bound group (it moves (1 + 1/p) S per GPU instead of 2(p-1)/p S, 1.56x less at
-    // p = 8; not measured on 8 GPUs here), else the TMA two-shot.
+    // 72/189/679, pushed 95/210/737, NCCL 70/186/685).  NVLS, when the caller allowed switch
+    // reduction (tolerance contract) and the group is multicast-bound: it moves (1 + 1/p) S per
+    // GPU each way instead of 2(p-1)/p S.  At p = 4 (ResNet-50 group) it ties the two-shot:
+    // allreduce 257 vs 257 us, fused SGD 289 vs 274 us -- per-direction rates 497 / 442 GB/s
+    // against 596 / 559 for the two-shot, so by bytes NVLS wins from p = 5 (allreduce: p > 4.0,
+    // SGD: p > 4.4); not measurable beyond 4 GPUs here.
     const bool nvls_ok = ga->d_mc != nullptr && op != OP_EASGD;
     // Low-latency (LL): every element travels once to every peer as an 8-byte {value, epoch}
     // word and is awaited in local memory -- no barrier round trip (small groups only).
@@ -442,10 +445,8 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     else if (c.algo_override == ALGO_TWOSHOT_TMA) algo = ALGO_TWOSHOT_TMA;
     else if (c.algo_override == ALGO_TWOSHOT_BAL) algo = ALGO_TWOSHOT_BAL;
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
-    // (automatic NVLS only for the plain allreduce: the fused SGD step's HBM epilogue cannot
-    // start before the switch has reduced a chunk, measured 405 us vs 297 us pulled at p = 4)
     else if (nvls_ok && (c.algo_override == ALGO_NVLS ||
-                         (c.allow_switch && p >= 6 && op == OP_ALLREDUCE)))
+                         (c.algo_override == 0 && c.allow_switch && p >= 5)))
       algo = ALGO_NVLS;
     // TMA-staged two-shot: ResNet-50 group p = 2 allreduce 188 / SGD step 197 us (LDG pull
     // 208 / 226, NCCL allreduce 219); p = 4 262 / 278 us (pull 289 / 301, NCCL 274-276).

@@ -113,6 +113,9 @@ def main():
     ap.add_argument("--carveout", action="store_true",
                     help="GEMM mode: leave the collective's CTAs free via cuBLASLt's SM carveout")
     ap.add_argument("--bucket-mb", type=float, default=64.0)
+    ap.add_argument("--green", type=int, default=0,
+                    help="run the backward pass in a CUDA green context of (SMs - GREEN) SMs, so "
+                         "GREEN SMs stay free for the collective (budget GREEN CTAs)")
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -174,19 +177,44 @@ def main():
     # bottleneck): a compute burst proportional to the bucket's bytes, then one copy writing the
     # bucket's gradients (contiguous views of the flat gradient buffer), last layers first.
 
+    gctx, gstream = None, None
+    if a.green:
+        from torch.cuda.green_contexts import GreenContext
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        gctx = GreenContext.create(sms - a.green, local)
+        gctx.set_context()
+        gs = gctx.Stream()
+        gctx.pop_context()
+        gstream = gs if isinstance(gs, torch.cuda.Stream) else torch.cuda.Stream(
+            stream_id=gs.stream_id, device_index=gs.device_index, device_type=gs.device_type)
+
     def backward(after=None):
-        for k in range(nb):
-            burst(k)
-            lo, hi = spans[k]
-            g_flat[lo:hi].copy_(gp_flat[lo:hi])
-            if after:
-                for t in reversed(members[k]):
-                    after(t)
+        """On the green stream when --green: the GEMMs (and gradient writes) then run on the
+        green context's SMs only; the caller's stream waits for it at the end."""
+        cur = torch.cuda.current_stream()
+        if gstream is not None:
+            gstream.wait_stream(cur)
+            gctx.set_context()
+        try:
+            with torch.cuda.stream(gstream if gstream is not None else cur):
+                for k in range(nb):
+                    burst(k)
+                    lo, hi = spans[k]
+                    g_flat[lo:hi].copy_(gp_flat[lo:hi])
+                    if after:
+                        for t in reversed(members[k]):
+                            after(t)
+        finally:
+            if gstream is not None:
+                gctx.pop_context()
+                cur.wait_stream(gstream)
 
     t_compute = timed(backward, a.iters, world)
     t_serial = timed(lambda: (backward(), whole_step()), a.iters, world)
     rows = []
-    for split, ctas in ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)):
+    shapes = (((False, a.green), (True, a.green)) if a.green else
+              ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)))
+    for split, ctas in shapes:
         step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas,
                                split=split)
         # GEMM mode: cuBLAS leaves `ctas` SMs to the collective (SM carveout), as a framework
@@ -195,7 +223,7 @@ def main():
         torch._C._set_sm_carveout_experimental(carve)
 
         def overlapped():
-            backward(lambda t: step.grad_ready(t, **hp))
+            backward(lambda t: step.grad_ready(t, torch.cuda.current_stream(), **hp))
             step.finish()
 
         t_comp_c = timed(backward, a.iters, world) if carve else t_compute
@@ -206,7 +234,7 @@ def main():
                      "mode": "split" if split else "fused",
                      "buckets": step.nbuckets, "bucket_mb": a.bucket_mb,
                      "ratio": a.ratio, "compute": a.compute, "compute_units": units,
-                     "sm_carveout": carve,
+                     "sm_carveout": carve, "green_context_sms_reserved": a.green or None,
                      "t_step_us": t_step, "t_compute_us": t_compute,
                      "t_compute_carveout_us": t_comp_c, "t_serial_us": t_serial,
                      "t_overlap_us": t_over,

@@ -175,6 +175,9 @@ def main():
                 _, Ws, Dws = O.sgd_step([w], [G], [dw], **hp)
                 assert_bitwise(to_host(dwt), Ws[0], "nvls sgd w")
                 assert_bitwise(to_host(ddw), Dws[0], "nvls sgd dw")
+        # tc_mem_free refuses while a live group still points into the allocation
+        st = tc.LIB.tc_mem_free(comm.h, sym.data_ptr())
+        assert st == tc.tc.TC_ERR_INVALID_ARG, st
     comm.free_symmetric(sym)
     assert comm.async_error() == 0
     if rank == 0:

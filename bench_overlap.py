@@ -177,26 +177,41 @@ def main():
     # bottleneck): a compute burst proportional to the bucket's bytes, then one copy writing the
     # bucket's gradients (contiguous views of the flat gradient buffer), last layers first.
 
-    gctx, gstream = None, None
+    gctx, gstream, cctx, cstream = None, None, None, None
     if a.green:
+        # green contexts: the backward pass on (SMs - GREEN) SMs, the collective's launches on the
+        # other GREEN SMs (kernels of the primary context and of a green context time-slice, so
+        # both sides get one)
         from torch.cuda.green_contexts import GreenContext
         sms = torch.cuda.get_device_properties(local).multi_processor_count
-        gctx = GreenContext.create(sms - a.green, local)
-        gctx.set_context()
-        gs = gctx.Stream()
-        gctx.pop_context()
-        gstream = gs if isinstance(gs, torch.cuda.Stream) else torch.cuda.Stream(
-            stream_id=gs.stream_id, device_index=gs.device_index, device_type=gs.device_type)
+
+        def green(n):
+            ctx = GreenContext.create(n, local)
+            ctx.set_context()
+            s = ctx.Stream()
+            ctx.pop_context()
+            s = s if isinstance(s, torch.cuda.Stream) else torch.cuda.Stream(
+                stream_id=s.stream_id, device_index=s.device_index, device_type=s.device_type)
+            return ctx, s
+        gctx, gstream = green(sms - a.green)
+        cctx, cstream = green(a.green)
 
     def backward(after=None):
-        """On the green stream when --green: the GEMMs (and gradient writes) then run on the
-        green context's SMs only; the caller's stream waits for it at the end."""
+        if gstream is None:
+            for k in range(nb):
+                burst(k)
+                lo, hi = spans[k]
+                g_flat[lo:hi].copy_(gp_flat[lo:hi])
+                if after:
+                    for t in reversed(members[k]):
+                        after(t)
+            return
+        # --green: the GEMMs and gradient writes on the green stream; the caller's stream waits
         cur = torch.cuda.current_stream()
-        if gstream is not None:
-            gstream.wait_stream(cur)
-            gctx.set_context()
+        gstream.wait_stream(cur)
+        gctx.set_context()
         try:
-            with torch.cuda.stream(gstream if gstream is not None else cur):
+            with torch.cuda.stream(gstream):
                 for k in range(nb):
                     burst(k)
                     lo, hi = spans[k]
@@ -205,9 +220,8 @@ def main():
                         for t in reversed(members[k]):
                             after(t)
         finally:
-            if gstream is not None:
-                gctx.pop_context()
-                cur.wait_stream(gstream)
+            gctx.pop_context()
+            cur.wait_stream(gstream)
 
     t_compute = timed(backward, a.iters, world)
     t_serial = timed(lambda: (backward(), whole_step()), a.iters, world)
@@ -216,14 +230,24 @@ def main():
               ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)))
     for split, ctas in shapes:
         step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas,
-                               split=split)
+                               split=split, stream=cstream)
         # GEMM mode: cuBLAS leaves `ctas` SMs to the collective (SM carveout), as a framework
         # overlapping communication with persistent GEMMs does
         carve = ctas if (a.compute == "gemm" and ctas and a.carveout) else None
         torch._C._set_sm_carveout_experimental(carve)
 
+        def ready(t):
+            if cctx is None:
+                return step.grad_ready(t, **hp)
+            cs = torch.cuda.current_stream()
+            cctx.set_context()  # the bucket's launch goes to the collective's green context
+            try:
+                step.grad_ready(t, cs, **hp)
+            finally:
+                cctx.pop_context()
+
         def overlapped():
-            backward(lambda t: step.grad_ready(t, torch.cuda.current_stream(), **hp))
+            backward(ready)
             step.finish()
 
         t_comp_c = timed(backward, a.iters, world) if carve else t_compute

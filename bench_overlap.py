@@ -113,6 +113,11 @@ def main():
     ap.add_argument("--carveout", action="store_true",
                     help="GEMM mode: leave the collective's CTAs free via cuBLASLt's SM carveout")
     ap.add_argument("--bucket-mb", type=float, default=64.0)
+    ap.add_argument("--algo", type=int, default=0,
+                    help="collective algorithm (1: register pull, no shared memory -- its CTAs "
+                         "can sit on an SM beside a GEMM CTA)")
+    ap.add_argument("--threads", type=int, default=0, help="threads per CTA (register kernels)")
+    ap.add_argument("--shapes", default="", help="ctas list for the overlap runs, e.g. 148,296")
     ap.add_argument("--green", type=int, default=0,
                     help="run the backward pass in a CUDA green context of (SMs - GREEN) SMs, so "
                          "GREEN SMs stay free for the collective (budget GREEN CTAs)")
@@ -142,7 +147,7 @@ def main():
     def whole_step():
         tc.sgd_step(Wg, G, D, **hp)
 
-    comm.set_tuning(0, 0, -1)
+    comm.set_tuning(0, a.threads, -1)
     t_step = timed(lambda: (g_flat.copy_(gp_flat), whole_step()), a.iters, world) - \
         timed(lambda: g_flat.copy_(gp_flat), a.iters, world)
     bucket_of, nb = tc.Plan(numels).buckets(int(a.bucket_mb * (1 << 20)))
@@ -226,8 +231,10 @@ def main():
     t_compute = timed(backward, a.iters, world)
     t_serial = timed(lambda: (backward(), whole_step()), a.iters, world)
     rows = []
+    comm.set_algorithm(a.algo)
     shapes = (((False, a.green), (True, a.green)) if a.green else
-              ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)))
+              tuple((sp, int(c)) for sp in (False, True) for c in a.shapes.split(",")) if a.shapes
+              else ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)))
     for split, ctas in shapes:
         step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas,
                                split=split, stream=cstream)
@@ -253,8 +260,9 @@ def main():
         t_comp_c = timed(backward, a.iters, world) if carve else t_compute
         t_over = timed(overlapped, a.iters, world)
         torch._C._set_sm_carveout_experimental(None)
-        comm.set_tuning(0, 0, -1)
+        comm.set_tuning(0, a.threads, -1)
         rows.append({"bench": "overlap (NEXT row f1)", "n_gpus": world, "ctas": ctas or "auto",
+                     "algo": step.comm.last_launch()[0], "threads": a.threads or None,
                      "mode": "split" if split else "fused",
                      "buckets": step.nbuckets, "bucket_mb": a.bucket_mb,
                      "ratio": a.ratio, "compute": a.compute, "compute_units": units,

@@ -1765,6 +1765,9 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #ifndef TC_NV_RW_SGD
 #define TC_NV_RW_SGD 4  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
 #endif
+#ifndef TC_NV_AR_CLAIM
+#define TC_NV_AR_CLAIM 0  // plain allreduce: tiles claimed from a per-rank counter
+#endif
 #ifndef TC_NV_FENCE
 #define TC_NV_FENCE 0   // 0: the signal warp fences; 1: every reduction warp fences its own
 #endif                  // stores (2: no fence -- timing experiments only, not ordered)
@@ -1924,6 +1927,45 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
   stamp(kp, 0);
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;  // every rank's data is in place
   stamp(kp, 1);
+#if TC_NV_AR_CLAIM
+  if constexpr (OP != OP_SGD) {
+    // plain allreduce: the reduction warps of every CTA claim the rank's tiles one at a time from
+    // a device counter (no CTA waits for a slower one); the last CTA of the rank to finish
+    // publishes the whole chunk on CTA 0's flag, and CTA 0 alone waits for every owner's
+    // (the kernel -- the call -- completes when CTA 0 does)
+    DevState* st = kp.state + r;
+    const int n_r = kp.tile2_off[r + 1] - kp.tile2_off[r];
+    if (warp < kNvlsWarps - 1) {
+      while (true) {
+        int i = 0;
+        if (lane_id == 0) i = (int)atomicAdd(&st->ctr_rs, 1u);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= n_r) break;
+        nv_reduce_tile<OP>(kp, nv_tile(kp, kp.tile2_off[r] + i), lane_id);
+      }
+    }
+    stamp(kp, 2);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      if (atomicAdd(&st->done_rs, 1u) == gridDim.x - 1) {
+        __threadfence_system();
+        for (int q = 0; q < P; ++q) st_release_sys(kp.flags[q] + flag_index(BAR_PROG, r, 0), nv_flag_value(1));
+      }
+    }
+    stamp(kp, 3);
+    bool ok = true;
+    if (b == 0 && warp == 0) {
+      if (lane_id < P) ok = nv_wait(kp, r, lane_id, 1);
+      ok = __all_sync(0xffffffffu, ok);
+    }
+    stamp(kp, 4);
+    if (!__syncthreads_and(ok)) return;
+    call_end(kp, r);
+    stamp(kp, 5);
+    return;
+  }
+#endif
   int cnt, tpr;
   nv_counts<OP>(kp, r, NW, cnt, tpr);
   const int nr = (cnt + tpr - 1) / tpr;

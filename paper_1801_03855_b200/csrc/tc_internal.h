@@ -89,9 +89,9 @@ constexpr int t2_smem(int op, int p) {
 
 constexpr int kNvlsThreads = 512;              // NVLS: 16 warps (reduction / signal / epilogue)
 #ifndef TC_NV_SLOTS
-#define TC_NV_SLOTS 256
+#define TC_NV_SLOTS 512
 #endif
-constexpr int kNvSlots = TC_NV_SLOTS;           // NVLS tile: <= 256 slots = 4 KiB per operand
+constexpr int kNvSlots = TC_NV_SLOTS;           // NVLS tile: <= 512 slots = 8 KiB per operand
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_PROG = 2, BAR_MID2 = 3 };  // PROG: NVLS rounds
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4, OP_EASYNC = 5 };
 enum Algo {

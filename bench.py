@@ -559,11 +559,17 @@ def main():
                                               "HBM epilogue overlapped per published round"}
             comm.set_algorithm(args.algo)
             refresh_g()
-        # tensor broadcast from rank 0 (weight initialisation): scatter + allgather
+        # tensor broadcast from rank 0 (weight initialisation): through the switch for
+        # the multicast-bound gradient bucket, else scatter + allgather (both timed)
         tb = timed_us(lambda: tc.broadcast(G, 0, stream=stream))
         extra["broadcast"] = {"t_us": tb, "algbw_gbs": S / tb / 1e3,
                               "busbw_gbs": S / tb / 1e3 * (p - 1) / p,
                               "algo": comm.last_launch()[0]}
+        if comm.last_launch()[0] == "nvls":
+            comm.set_algorithm(6)
+            tb2 = timed_us(lambda: tc.broadcast(G, 0, stream=stream))
+            extra["broadcast"]["two_shot_t_us"] = tb2
+            comm.set_algorithm(args.algo)
         if not args.no_nccl:
             import torch.distributed as dist
             flat = torch.empty(sum(numels), dtype=torch.float32, device="cuda")

@@ -2054,6 +2054,62 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
   stamp(kp, 5);
 }
 
+// Tensor broadcast through the switch (ALGO_NVLS, multicast-bound groups): the root reads its
+// tensors and writes every rank's copy with one multimem.st per 16 B -- each byte leaves the root
+// once (egress S, every rank's ingress S) instead of the scatter + allgather's 2(p-1)/p S out of
+// the root.  A copy, so bit-exact.  ENTRY barrier (no rank still uses its old values); tile i of
+// the whole group on CTA i mod grid, warps round-robin; the root's CTA b fences and publishes,
+// every other rank's CTA b waits for it (the call completes once every tile has landed).
+template <int P>
+__global__ void __launch_bounds__(kNvlsThreads, 1) k_nvls_bcast(KParams kp) {
+  const int r = kp.rank0 + (int)blockIdx.y;
+  if (r == kp.absent_rank) return;
+  call_begin(kp, r);
+  const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  const int b = (int)blockIdx.x, G = (int)gridDim.x;
+  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
+  bool ok = true;
+  if (r == kp.root) {
+    const int n = kp.tile2_off[P] - kp.tile2_off[0];
+    const size_t row = (size_t)r * kp.T;
+    for (int k = warp; b + G * k < n; k += kNvlsWarps) {
+      const NvTile d = nv_tile(kp, kp.tile2_off[0] + b + G * k);
+      const float* src = kp.a[row + d.t] + d.e;
+      float* mc = kp.mc[d.t] + d.e;
+      if (d.full && ((((uintptr_t)src | (uintptr_t)mc) & 15) == 0)) {
+        constexpr int U = 4;
+        for (int s0 = lane_id; s0 < d.n; s0 += 32 * U) {
+          float4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (s0 + 32 * u < d.n) v[u] = ld16(src + 4 * (s0 + 32 * u));
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (s0 + 32 * u < d.n) mm_st16(mc + 4 * (s0 + 32 * u), v[u]);
+        }
+      } else {
+        const int64_t j0 = d.e < 0 ? -d.e : 0;
+        const int64_t j1 = min(4 * (int64_t)d.n, kp.numel[d.t] - d.e);
+        for (int64_t j = j0 + lane_id; j < j1; j += 32) mm_st4(mc + j, ld4(src + j));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int q = 0; q < P; ++q)
+        if (q != r)
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(
+                           kp.flags[q] + flag_index(BAR_PROG, r, b)),
+                       "r"(nv_flag_value(1))
+                       : "memory");
+    }
+  } else if (threadIdx.x == 0) {
+    ok = nv_wait(kp, r, kp.root, 1);
+  }
+  if (!__syncthreads_and(ok)) return;
+  call_end(kp, r);
+}
+
 template <int OP>
 const void* kernel_ptr(int algo, int p) {
   if (algo == ALGO_LOCAL) return (const void*)k_local_tma<OP>;

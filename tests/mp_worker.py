@@ -175,6 +175,18 @@ def main():
                 _, Ws, Dws = O.sgd_step([w], [G], [dw], **hp)
                 assert_bitwise(to_host(dwt), Ws[0], "nvls sgd w")
                 assert_bitwise(to_host(ddw), Dws[0], "nvls sgd dw")
+        # tensor broadcast through the switch (a copy: bit-exact), chosen automatically for a
+        # multicast-bound group; the TMA scatter + allgather when forced
+        for algo, want in ((0, "nvls" if comm.multicast_supported else "two-shot-tma"),
+                           (6, "two-shot-tma")):
+            comm.set_algorithm(algo)
+            xs = [W.group(numels, "grad", 65, algo, k, W.GRAD) for k in range(p)]
+            for v, a in zip(views, xs[rank]):
+                v.copy_(torch.from_numpy(a))
+            tc.broadcast(g, p - 1)
+            assert comm.last_launch()[0] == want, comm.last_launch()
+            assert_bitwise(to_host(views), O.broadcast(xs, p - 1)[rank], f"broadcast {want}")
+        comm.set_algorithm(0)
         # tc_mem_free refuses while a live group still points into the allocation
         st = tc.LIB.tc_mem_free(comm.h, sym.data_ptr())
         assert st == tc.tc.TC_ERR_INVALID_ARG, st

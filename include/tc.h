@@ -313,11 +313,13 @@ TC_API tc_status tc_easgd_async_update(tc_group* x, tc_group* center, float alph
                                        const int* order, void* stream);
 
 /* Tensor broadcast (MPI_Bcast of the weights at initialisation; the KVStore.pull
- * broadcast): every rank's group := the root's group, bit for bit.  Scatter from
- * the root (each rank copies its owner chunk of the root's tensors) then the allgather of the
- * two-shot, so every GPU receives S bytes and the root sends S.  Collective; root identical on
- * all ranks.  p = 1: no-op.  Errors: TC_ERR_INVALID_ARG (root outside [0, nranks)),
- * TC_ERR_TIMEOUT, TC_ERR_BUSY, TC_ERR_CUDA. */
+ * broadcast): every rank's group := the root's group, bit for bit.  Groups in
+ * multicast-bound tc_mem_alloc memory at p >= 4 (or with tc_comm_set_algorithm(4)): the root
+ * writes every rank's copy with NVSwitch multicast stores (each byte leaves the root once; a
+ * copy, so exact).  Otherwise: scatter from the root (each rank copies its owner
+ * chunk of the root's tensors) then the allgather of the two-shot (the root sends
+ * 2(p-1)/p S).  Collective; root identical on all ranks.  p = 1: no-op.  Errors:
+ * TC_ERR_INVALID_ARG (root outside [0, nranks)), TC_ERR_TIMEOUT, TC_ERR_BUSY, TC_ERR_CUDA. */
 TC_API tc_status tc_broadcast(tc_group* x, int root, void* stream);
 
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):

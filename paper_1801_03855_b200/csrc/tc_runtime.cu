@@ -402,9 +402,11 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (p == 1) {
     algo = ALGO_LOCAL;
   } else if (op == OP_BCAST) {
-    // a copy, so the switch path is bit-exact: multicast-bound groups take it (the root's bytes
-    // leave it once: p = 4 ResNet-50 group XXX us vs 246 for the scatter + allgather)
-    const bool mc = ga->d_mc != nullptr && c.algo_override != ALGO_TWOSHOT_TMA;
+    // a copy, so the switch path is bit-exact.  Multicast-bound groups take it from p = 4: the
+    // root's bytes leave it once (S at ~480 GB/s: ResNet-50 group 214.5 us at p = 4 vs 246 for
+    // the scatter + allgather, whose root sends 2(p-1)/p S; at p = 2 it loses, 212 vs 165 us)
+    const bool mc = ga->d_mc != nullptr &&
+                    (c.algo_override == ALGO_NVLS || (c.algo_override == 0 && p >= 4));
     algo = mc ? ALGO_NVLS : ALGO_TWOSHOT_TMA;
     if (!mc && (Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   } else if (op == OP_EASYNC) {  // implemented by the TMA two-shot only

@@ -177,8 +177,9 @@ def main():
                 assert_bitwise(to_host(ddw), Dws[0], "nvls sgd dw")
         # tensor broadcast through the switch (a copy: bit-exact), chosen automatically for a
         # multicast-bound group; the TMA scatter + allgather when forced
-        for algo, want in ((0, "nvls" if comm.multicast_supported else "two-shot-tma"),
-                           (6, "two-shot-tma")):
+        mc = comm.multicast_supported
+        for algo, want in ((0, "nvls" if mc and p >= 4 else "two-shot-tma"),
+                           (4, "nvls" if mc else "two-shot-tma"), (6, "two-shot-tma")):
             comm.set_algorithm(algo)
             xs = [W.group(numels, "grad", 65, algo, k, W.GRAD) for k in range(p)]
             for v, a in zip(views, xs[rank]):

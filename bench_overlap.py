@@ -118,6 +118,8 @@ def main():
                          "can sit on an SM beside a GEMM CTA)")
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (register kernels)")
     ap.add_argument("--shapes", default="", help="ctas list for the overlap runs, e.g. 148,296")
+    ap.add_argument("--priority", action="store_true",
+                    help="the collective's side stream at the highest stream priority")
     ap.add_argument("--green", type=int, default=0,
                     help="run the backward pass in a CUDA green context of (SMs - GREEN) SMs, so "
                          "GREEN SMs stay free for the collective (budget GREEN CTAs)")
@@ -236,8 +238,12 @@ def main():
               tuple((sp, int(c)) for sp in (False, True) for c in a.shapes.split(",")) if a.shapes
               else ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)))
     for split, ctas in shapes:
+        side = cstream
+        if side is None and a.priority:
+            lo, hi = torch.cuda.Stream.priority_range()
+            side = torch.cuda.Stream(priority=hi)
         step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas,
-                               split=split, stream=cstream)
+                               split=split, stream=side)
         # GEMM mode: cuBLAS leaves `ctas` SMs to the collective (SM carveout), as a framework
         # overlapping communication with persistent GEMMs does
         carve = ctas if (a.compute == "gemm" and ctas and a.carveout) else None
@@ -267,6 +273,7 @@ def main():
                      "buckets": step.nbuckets, "bucket_mb": a.bucket_mb,
                      "ratio": a.ratio, "compute": a.compute, "compute_units": units,
                      "sm_carveout": carve, "green_context_sms_reserved": a.green or None,
+                     "side_stream_priority": bool(a.priority),
                      "t_step_us": t_step, "t_compute_us": t_compute,
                      "t_compute_carveout_us": t_comp_c, "t_serial_us": t_serial,
                      "t_overlap_us": t_over,

@@ -102,11 +102,8 @@ enum Algo {
   ALGO_NVLS = 4,
   ALGO_LL = 5,
   ALGO_TWOSHOT_TMA = 6,
-  ALGO_TWOSHOT_BAL = 7,
-  ALGO_ONESHOT_DIRECT = 8
+  ALGO_TWOSHOT_BAL = 7
 };
-// one-shot without staging: slots each thread keeps in shared memory (512 threads x 16 B each)
-constexpr int kDirectMaxSlotsPerThread = 24;    // 192 KiB per CTA
 
 // ---------------------------------------------------------------- A1 descriptor (host)
 struct Plan {

@@ -34,7 +34,6 @@ Shape shape_of(int op, int algo, int p, int threads) {
     return {kTmaThreads, op == OP_ESGD ? kTmaSmem4 : kTmaSmem};
   if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL) return {kT2Threads, t2_smem(op, p)};
   if (algo == ALGO_NVLS) return {kNvlsThreads, 0};
-  if (algo == ALGO_ONESHOT_DIRECT) return {512, kDirectMaxSlotsPerThread * 16 * 512};
   return {threads, 0};
 }
 

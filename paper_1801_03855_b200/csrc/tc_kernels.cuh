@@ -838,113 +838,6 @@ __global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
   stamp(kp, 5);
 }
 
-// One-shot without staging (ALGO_ONESHOT_DIRECT): every rank reduces its CTA's pieces of the
-// whole group straight from every rank's tensors (remote 16-B loads), keeps the reduced primary
-// values in shared memory, and writes them in place only after the EXIT barrier (every rank's
-// counterpart CTA has read this rank's tensors); operands nobody else reads (w, dw, the center)
-// are written at once.  Saves the one-shot's staging copy and its HBM round trip.  Each thread
-// keeps its slots' results at res[i * blockDim + tid] in the order slot_loop hands them out.
-template <int OP, int P>
-struct DirectBody {
-  using N = Needs<OP, PH_RS, P>;
-  static constexpr int NP = 3 + P;
-  const KParams& kp;
-  int r;
-  float4* res;
-  int* idx;
-  struct State {
-    float4 x[P];
-    float4 b, c;
-    float *pb, *pc;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const {
-    const size_t mine = (size_t)r * kp.T + t;
-    ptr[0] = kp.a[mine];
-    ptr[1] = (N::loadB || N::storeB) ? kp.b[mine] : nullptr;
-    ptr[2] = (N::loadC || N::storeC) ? kp.c[mine] : nullptr;
-#pragma unroll
-    for (int k = 0; k < P; ++k) ptr[3 + k] = kp.a[(size_t)k * kp.T + t];
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef& ref, float* const* ptr, State& st) const {
-#pragma unroll
-    for (int k = 0; k < P; ++k) st.x[k] = ldv<VEC>(ptr[3 + k], ref);
-    if constexpr (N::loadB) st.b = ldv<VEC>(ptr[1], ref);
-    if constexpr (N::loadC) st.c = ldv<VEC>(ptr[2], ref);
-    st.pb = ptr[1];
-    st.pc = ptr[2];
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-    float4 oa;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float in[P];
-#pragma unroll
-      for (int k = 0; k < P; ++k) in[k] = lane(st.x[k], i);
-      float la = 0.f;
-      float lb = N::loadB ? lane(st.b, i) : 0.f;
-      float lc = N::loadC ? lane(st.c, i) : 0.f;
-      elem<OP, PH_RS, P>(kp, r, in, la, lb, lc);
-      lane(oa, i) = la;
-      if constexpr (N::storeB) lane(st.b, i) = lb;
-      if constexpr (N::storeC) lane(st.c, i) = lc;
-    }
-    if constexpr (N::storeB) stv<VEC>(st.pb, ref, st.b);
-    if constexpr (N::storeC) stv<VEC>(st.pc, ref, st.c);
-    res[(size_t)(*idx)++ * blockDim.x + threadIdx.x] = oa;
-  }
-};
-
-struct WriteBackBody {
-  static constexpr int NP = 1;
-  const KParams& kp;
-  int r;
-  const float4* res;
-  int* idx;
-  struct State {
-    float* pa;
-  };
-  __device__ __forceinline__ void bind(int t, float** ptr) const {
-    ptr[0] = kp.a[(size_t)r * kp.T + t];
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void load(const SlotRef&, float* const* ptr, State& st) const {
-    st.pa = ptr[0];
-  }
-  template <bool VEC>
-  __device__ __forceinline__ void finish(const SlotRef& ref, State& st) const {
-    stv<VEC>(st.pa, ref, res[(size_t)(*idx)++ * blockDim.x + threadIdx.x]);
-  }
-};
-
-template <int OP, int P>
-__global__ void __launch_bounds__(512, 1) k_oneshot_direct(KParams kp) {
-  extern __shared__ __align__(16) float4 res[];
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  stamp(kp, 0);
-  if (!barrier_all(kp, r, BAR_ENTRY, true)) return;  // every rank's data is in place
-  stamp(kp, 1);
-  int idx = 0;
-  {
-    DirectBody<OP, P> body{kp, r, res, &idx};
-    slot_loop<1>(kp, 0, kp.M, body);
-  }
-  stamp(kp, 2);
-  if (!barrier_all(kp, r, BAR_MID, true)) return;  // every counterpart has read my tensors
-  stamp(kp, 3);
-  idx = 0;
-  {
-    WriteBackBody body{kp, r, res, &idx};
-    slot_loop<1>(kp, 0, kp.M, body);
-  }
-  stamp(kp, 4);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
 // Low-latency: no barrier; each slot is pushed to every peer and its peers' words awaited.
 template <int OP, int P, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_ll(KParams kp) {
@@ -2228,7 +2121,6 @@ const void* kernel_ptr(int algo, int p) {
     if (algo == ALGO_TWOSHOT_TMA) return (const void*)k_twoshot_tma<OP, PP>;                 \
     if (algo == ALGO_TWOSHOT_BAL) return (const void*)k_twoshot_bal<OP, PP>;                 \
     if (algo == ALGO_LL) return (const void*)k_ll<OP, PP, 2>;                                \
-    if (algo == ALGO_ONESHOT_DIRECT) return (const void*)k_oneshot_direct<OP, PP>;           \
     return algo == ALGO_TWOSHOT        ? (const void*)k_twoshot_pull<OP, PP, 2>              \
            : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 2>              \
                                        : (const void*)k_oneshot<OP, PP, 2>;

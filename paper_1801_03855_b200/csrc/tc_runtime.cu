@@ -444,15 +444,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     const int64_t ll_cap = (int64_t)(kLLBytes / 2 / 8 / p) & ~(size_t)3;
     const int64_t ll_auto = p == 2 ? kDefaultLLMax : (p <= 4 ? kDefaultLLMax / 2 : kDefaultLLMax / 8);
     const int64_t ll_lim = c.tune_ll < 0 ? ll_auto : c.tune_ll;
-    // one-shot without staging: the reduced values of every slot wait in shared memory, so the
-    // group must fit (slots per thread of the piece deal on a one-CTA-per-SM grid)
-    const int64_t dgrid = std::max(1, c.num_sms / (c.emulated ? p : 1));
-    const int64_t dpieces = (Mdev + kPiece - 1) / kPiece;
-    const bool direct_fits =
-        (dpieces + dgrid * 16 - 1) / (dgrid * 16) * (kPiece / 32) <= kDirectMaxSlotsPerThread;
-    if (c.algo_override == ALGO_ONESHOT_DIRECT && direct_fits && op != OP_ESGD)
-      algo = ALGO_ONESHOT_DIRECT;
-    else if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
+    if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
     else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;
     else if (c.algo_override == ALGO_TWOSHOT_PUSH) algo = ALGO_TWOSHOT_PUSH;
     else if (c.algo_override == ALGO_TWOSHOT_TMA) algo = ALGO_TWOSHOT_TMA;
@@ -492,8 +484,6 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
                                                 : c.num_sms * occ);
     kp.tiles = ga->d_tiles;
     kp.ntiles = ga->ntiles;
-  } else if (algo == ALGO_ONESHOT_DIRECT) {  // one CTA per SM: the grid the fit was checked on
-    ctas = (int)std::max<int64_t>(1, c.num_sms / nlocal);
   } else if (twoshot && tune_ctas > 0) {
     ctas = tune_ctas;
   } else {
@@ -650,8 +640,7 @@ tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes) {
 
 tc_status tc_comm_set_algorithm(tc_comm* comm, int algo) {
   if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH &&
-                algo != ALGO_NVLS && algo != ALGO_TWOSHOT_TMA && algo != ALGO_TWOSHOT_BAL &&
-                algo != ALGO_ONESHOT_DIRECT))
+                algo != ALGO_NVLS && algo != ALGO_TWOSHOT_TMA && algo != ALGO_TWOSHOT_BAL))
     return TC_ERR_INVALID_ARG;
   comm->c.algo_override = algo;
   return TC_OK;

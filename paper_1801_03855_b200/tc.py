@@ -28,7 +28,7 @@ STATUS = {
 TC_OK, TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_NOT_SHAREABLE = 0, 1, 2, 3
 TC_ERR_BUSY, TC_ERR_TIMEOUT, TC_ERR_CUDA, TC_ERR_BOOTSTRAP, TC_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
 ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 3: "two-shot-push", 4: "nvls", 5: "ll",
-              6: "two-shot-tma", 7: "two-shot-bal", 8: "one-shot-direct"}
+              6: "two-shot-tma", 7: "two-shot-bal"}
 ALGO_AUTO, ALGO_TWOSHOT_PULL, ALGO_TWOSHOT_PUSH, ALGO_NVLS, ALGO_TWOSHOT_TMA = 0, 1, 3, 4, 6
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,

@@ -29,9 +29,8 @@ PUSH = -2           # force two-shot with pushed reduce-scatter
 LL = -3             # force the low-latency algorithm
 TMA = -4            # force the TMA-staged two-shot
 BAL = -5            # force the TMA two-shot with claimed (balanced) tiles
-DIRECT = -6         # force the one-shot without staging (results held in shared memory)
 ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT), ("ll", LL),
-         ("two-shot-tma", TMA), ("two-shot-bal", BAL), ("one-shot-direct", DIRECT)]
+         ("two-shot-tma", TMA), ("two-shot-bal", BAL)]
 
 
 def _comm(p, oneshot=-1, ctas=0):
@@ -49,9 +48,6 @@ def _comm(p, oneshot=-1, ctas=0):
         oneshot = 0
     elif oneshot == BAL:
         c.set_algorithm(7)
-        oneshot = 0
-    elif oneshot == DIRECT:
-        c.set_algorithm(8)
         oneshot = 0
     elif oneshot == TWOSHOT and p > 1:
         c.set_algorithm(1)
@@ -115,7 +111,7 @@ def test_unaligned_tensors(p, offset):
     numels = [7, 13, 1000, 4096, 3, 1, 2]
     xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
     off = (lambda k: k % 4) if offset == "per-rank" else offset
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL, DIRECT):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL):
         out, _ = run_allreduce(xs, oneshot=oneshot, offset=off)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -154,7 +150,7 @@ def test_fewer_slots_than_ranks(p):
     """N < p: some owners have empty chunks."""
     numels = [1, 2] if p == 4 else [3, 0, 1]
     xs = [W.group(numels, "int", 75, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, TMA, BAL, DIRECT):
+    for oneshot in (TWOSHOT, PUSH, TMA, BAL):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -165,7 +161,7 @@ def test_many_tensors_1024():
     g = np.random.default_rng(5)
     numels = W.random_numels(g, 1024, 700)
     xs = [W.group(numels, "grad", 74, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL, DIRECT):
+    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -441,7 +437,7 @@ def test_config5_sweep_shapes(p, T):
         if not numels:
             continue
         xs = [W.group(numels, "grad", W.CFG_SWEEP, 0, k, W.GRAD) for k in range(p)]
-        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL, TMA, BAL, DIRECT)):
+        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL, TMA, BAL)):
             if oneshot == LL and total > (64 << 10):
                 continue
             comm = _comm(p, oneshot)

@@ -30,11 +30,14 @@ def main():
     comm = tc.Comm.from_process_group(device=local)
     big = 64 << 20
     variants = [("auto", 0, 0, 0, -1, -1), ("ll", 0, 0, 0, -1, big),
-                ("tma", 6, 0, 0, 0, 0)]
-    for ctas in (16, 32, 64, 96, 148):
-        for thr in (256, 512):
-            variants.append((f"oneshot_c{ctas}_t{thr}", 0, ctas, thr, big, 0))
-    for total in (256 << 10, 512 << 10, 1 << 20, 2 << 20, 4 << 20):
+                ("tma", 6, 0, 0, 0, 0), ("oneshot", 0, 0, 0, big, 0)]
+    if os.environ.get("LAT_SHAPES"):
+        for ctas in (16, 32, 64, 96, 148):
+            for thr in (256, 512):
+                variants.append((f"oneshot_c{ctas}_t{thr}", 0, ctas, thr, big, 0))
+    sizes = [int(x) << 10 for x in os.environ.get(
+        "LAT_KIB", "16,64,256,512,1024,2048,4096,8192,16384").split(",")]
+    for total in sizes:
         N = total // 4
         flat = torch.randn(N, device="cuda")
         nccl_buf = torch.randn(N, device="cuda")

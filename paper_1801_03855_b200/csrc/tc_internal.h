@@ -18,7 +18,7 @@ namespace tc {
 
 constexpr int kMaxRanks = TC_MAX_RANKS;
 constexpr int kMaxCtas = 1024;                 // per barrier and source rank
-constexpr int kNumBarriers = 4;                // entry, mid, NVLS progress, mid (2nd half)
+constexpr int kNumBarriers = 3;                // entry, mid, NVLS progress
 constexpr size_t kFlagWords = (size_t)kNumBarriers * kMaxRanks * kMaxCtas;
 constexpr size_t kStageCapacity = 8u << 20;    // one-shot staging bytes per parity
 constexpr size_t kLLBytes = 16u << 20;         // low-latency receive buffers (after staging)
@@ -57,9 +57,6 @@ constexpr int kT2Slots = TC_T2_SLOTS;
 constexpr int t2_slots(int p) { return p == 2 ? 2 * kT2Slots : kT2Slots; }
 constexpr int kT2SmemCap = TC_T2_SMEM;
 constexpr int kT2MaxStages = 16;
-#ifndef TC_T2_SPLIT
-#define TC_T2_SPLIT 1  // 2: reduce-scatter / allgather in two published halves (see t2_phase)
-#endif
 #ifndef TC_T2_CW
 #define TC_T2_CW 8
 #endif
@@ -92,7 +89,7 @@ constexpr int kNvlsThreads = 512;              // NVLS: 16 warps (reduction / si
 #define TC_NV_SLOTS 512
 #endif
 constexpr int kNvSlots = TC_NV_SLOTS;           // NVLS tile: <= 512 slots = 8 KiB per operand
-enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_PROG = 2, BAR_MID2 = 3 };  // PROG: NVLS rounds
+enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_PROG = 2 };  // PROG: NVLS round progress
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4, OP_EASYNC = 5 };
 enum Algo {
   ALGO_LOCAL = 0,

@@ -1246,62 +1246,23 @@ __device__ __forceinline__ void t2_tile(const KParams& kp, int r, const T2Desc& 
   }
 }
 
-// Split phases (TC_T2_SPLIT == 2): every phase runs in two halves of this CTA's tiles of a chunk
-// (part 0: the first ceil(cnt/2), part 1: the rest; part -1: all).  The reduce-scatter's halves
-// are published separately (the last consumer warp to finish a half fences at system scope and
-// stores the epoch into every peer's flag sig_bar), and the producer waits for the peers' flag
-// wait_bar only before it issues the first allgather copies of that half: a CTA pair's skew in
-// the first half is hidden behind the second half's reduce-scatter, the second half's behind the
-// first half's allgather.
-template <int P>
-__device__ __forceinline__ bool t2_wait_peers(const KParams& kp, int r, int bar) {
-  const int lane_id = threadIdx.x & 31;
-  bool ok = true;
-  if (lane_id < P && lane_id != r) {
-    const uint32_t* f = kp.flags[r] + flag_index(bar, lane_id, blockIdx.x);
-    if ((int32_t)(ld_acquire_sys(f) - ep()) < 0) {
-      const unsigned long long t0 = globaltimer();
-      while ((int32_t)(ld_acquire_sys(f) - ep()) < 0)
-        if (globaltimer() - t0 > kp.timeout_ns) {
-          atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
-          ok = false;
-          break;
-        }
-    }
-  }
-  ok = __all_sync(0xffffffffu, ok);
-  if (lane_id == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-  __syncwarp();
-  return ok;
-}
-
 template <int OP, int P, int PH, int G, int OPSP, int OPS, int NS>
 __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float* stagebuf,
                                          int& k, uint64_t* full, uint64_t* empty,
                                          T2Desc (*desc)[8], float4* sm4,
-                                         unsigned long long& waited, int part = -1,
-                                         int wait_bar = -1, int sig_bar = -1,
-                                         uint32_t* sig_count = nullptr) {
+                                         unsigned long long& waited) {
   using N = Needs<OP, PH, PH == PH_RS ? P : 2>;
   constexpr int V = t2_slots(P);
   const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   const size_t T = (size_t)kp.T;
   const int lo = (int)((int64_t)kp.M * qo / P);
   const int first = kp.tile2_off[qo] + (int)blockIdx.x, end = kp.tile2_off[qo + 1];
-  const int ntot = first < end ? (end - first + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-  const int kb = part == 1 ? (ntot + 1) / 2 : 0;
-  const int cnt = part == 0 ? (ntot + 1) / 2 : ntot;  // this phase: j in [kb, cnt)
+  const int cnt = first < end ? (end - first + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   auto stage = [&](int s, int o) { return sm4 + ((size_t)s * OPS + o) * V; };
   if (warp == 0) {
-    if (wait_bar >= 0) {
-      // on a timeout (sticky TC_ERR_TIMEOUT) the phase still runs, so the consumers, who wait
-      // on the stage ring, are released; the comm is unusable afterwards anyway
-      t2_wait_peers<P>(kp, r, wait_bar);
-    } else {
-      if (lane_id == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-      __syncwarp();
-    }
-    for (int base = kb; base < cnt; base += 32) {
+    if (lane_id == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+    for (int base = 0; base < cnt; base += 32) {
       const int j = base + lane_id;
       const bool valid = j < cnt;
       T2Desc d{};
@@ -1385,7 +1346,7 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
   }
   // consumers
   const int ct = threadIdx.x - 32, nct = kT2Threads - 32;
-  for (int base = kb; base < cnt; base += 32) {
+  for (int base = 0; base < cnt; base += 32) {
     const int bc = min(32, cnt - base);
     for (int u0 = 0; u0 < bc; u0 += G) {
       const int s = k % NS;
@@ -1402,25 +1363,6 @@ __device__ __forceinline__ void t2_phase(const KParams& kp, int r, int qo, float
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
                      : "memory");
       ++k;
-    }
-  }
-  if (sig_bar >= 0) {  // the last consumer warp to finish this half publishes it
-    __syncwarp();
-    if (lane_id == 0) {
-      uint32_t old;
-      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                   : "=r"(old)
-                   : "r"(smem_u32(sig_count))
-                   : "memory");
-      if (old == kT2ConsumerWarps - 1) {
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-        for (int q = 0; q < P; ++q)
-          if (q != r)
-            asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(
-                             kp.flags[q] + flag_index(sig_bar, r, blockIdx.x)),
-                         "r"(ep())
-                         : "memory");
-      }
     }
   }
 }
@@ -1454,26 +1396,6 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
   stamp(kp, 1);
   int k = 0;  // position in the stage ring (continues across phases)
   unsigned long long waited = 0;  // profiling: producer waits for empty / consumers for full
-#if TC_T2_SPLIT == 2
-  __shared__ uint32_t s_half[2];
-  if (threadIdx.x < 2) s_half[threadIdx.x] = 0;
-  __syncthreads();
-  for (int h = 0; h < 2; ++h)  // reduce-scatter halves, each published on its own flag
-    t2_phase<OP, P, PH_RS, G_RS, OPS_RS, OPS, NS>(kp, r, r, arena_stage(kp, r, par), k, full,
-                                                   empty, desc, sm4, waited, h, -1,
-                                                   h ? BAR_MID2 : BAR_MID, s_half + h);
-  stamp(kp, 2);
-  stamp(kp, 3);
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll 1
-    for (int jq = 0; jq < P - 1; ++jq) {
-      const int qo = (r + 1 + jq) % P;
-      t2_phase<OP, P, PH_AG, G_AG, OPS_AG, OPS, NS>(kp, r, qo, arena_stage(kp, qo, par), k,
-                                                     full, empty, desc, sm4, waited, h,
-                                                     jq == 0 ? (h ? BAR_MID2 : BAR_MID) : -1);
-    }
-  }
-#else
   t2_phase<OP, P, PH_RS, G_RS, OPS_RS, OPS, NS>(kp, r, r, arena_stage(kp, r, par), k, full,
                                                  empty, desc, sm4, waited);
   stamp(kp, 2);
@@ -1485,7 +1407,6 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
     t2_phase<OP, P, PH_AG, G_AG, OPS_AG, OPS, NS>(kp, r, qo, arena_stage(kp, qo, par), k, full,
                                                    empty, desc, sm4, waited);
   }
-#endif
   stamp(kp, 4);
   if (kp.prof != nullptr && threadIdx.x < 32)  // producer lanes each timed their own waits
     for (int o = 16; o > 0; o >>= 1) waited += __shfl_xor_sync(0xffffffffu, waited, o);
@@ -1765,12 +1686,6 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #ifndef TC_NV_RW_SGD
 #define TC_NV_RW_SGD 4  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
 #endif
-#ifndef TC_NV_AR_CLAIM
-#define TC_NV_AR_CLAIM 0  // plain allreduce: tiles claimed from a per-rank counter
-#endif
-#ifndef TC_NV_FENCE
-#define TC_NV_FENCE 0   // 0: the signal warp fences; 1: every reduction warp fences its own
-#endif                  // stores (2: no fence -- timing experiments only, not ordered)
 #ifndef TC_NV_RED_U_SGD
 #define TC_NV_RED_U_SGD 4  // fused SGD: switch reductions in flight per lane
 #endif
@@ -1927,45 +1842,6 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
   stamp(kp, 0);
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;  // every rank's data is in place
   stamp(kp, 1);
-#if TC_NV_AR_CLAIM
-  if constexpr (OP != OP_SGD) {
-    // plain allreduce: the reduction warps of every CTA claim the rank's tiles one at a time from
-    // a device counter (no CTA waits for a slower one); the last CTA of the rank to finish
-    // publishes the whole chunk on CTA 0's flag, and CTA 0 alone waits for every owner's
-    // (the kernel -- the call -- completes when CTA 0 does)
-    DevState* st = kp.state + r;
-    const int n_r = kp.tile2_off[r + 1] - kp.tile2_off[r];
-    if (warp < kNvlsWarps - 1) {
-      while (true) {
-        int i = 0;
-        if (lane_id == 0) i = (int)atomicAdd(&st->ctr_rs, 1u);
-        i = __shfl_sync(0xffffffffu, i, 0);
-        if (i >= n_r) break;
-        nv_reduce_tile<OP>(kp, nv_tile(kp, kp.tile2_off[r] + i), lane_id);
-      }
-    }
-    stamp(kp, 2);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-      if (atomicAdd(&st->done_rs, 1u) == gridDim.x - 1) {
-        __threadfence_system();
-        for (int q = 0; q < P; ++q) st_release_sys(kp.flags[q] + flag_index(BAR_PROG, r, 0), nv_flag_value(1));
-      }
-    }
-    stamp(kp, 3);
-    bool ok = true;
-    if (b == 0 && warp == 0) {
-      if (lane_id < P) ok = nv_wait(kp, r, lane_id, 1);
-      ok = __all_sync(0xffffffffu, ok);
-    }
-    stamp(kp, 4);
-    if (!__syncthreads_and(ok)) return;
-    call_end(kp, r);
-    stamp(kp, 5);
-    return;
-  }
-#endif
   int cnt, tpr;
   nv_counts<OP>(kp, r, NW, cnt, tpr);
   const int nr = (cnt + tpr - 1) / tpr;
@@ -1975,10 +1851,6 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
       for (int k = j * tpr + warp; k < min(cnt, (j + 1) * tpr); k += NW)
         nv_reduce_tile<OP>(kp, nv_tile(kp, kp.tile2_off[r] + b + G * k), lane_id);
       __syncwarp();
-#if TC_NV_FENCE == 1
-      // each reduction warp makes its own stores visible system-wide before the round closes
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-#endif
       // every reduction warp syncs too: a warp must not arrive twice at one barrier phase
       asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
     }
@@ -1987,19 +1859,12 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
     for (int j = 0; j < nr; ++j) {
       asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
       if (lane_id == 0) {
-#if TC_NV_FENCE == 0
         asm volatile("fence.acq_rel.sys;" ::: "memory");
-#endif
-        for (int q = 0; q < P; ++q) {
-#if TC_NV_FENCE == 1
-          st_release_sys(kp.flags[q] + flag_index(BAR_PROG, r, b), nv_flag_value(j + 1));
-#else
+        for (int q = 0; q < P; ++q)
           asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(
                            kp.flags[q] + flag_index(BAR_PROG, r, b)),
                        "r"(nv_flag_value(j + 1))
                        : "memory");
-#endif
-        }
       }
       __syncwarp();
     }

@@ -56,6 +56,8 @@ def main():
                         ev[i - 5][0].record(s)
                     if op == "ar":
                         tc.allreduce(G, 1.0 / p, stream=s)
+                    elif op == "bc":
+                        tc.broadcast(G, 0, stream=s)
                     else:
                         tc.sgd_step(Wg, G, D, lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (128 * p),
                                     stream=s)

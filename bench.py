@@ -396,7 +396,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true",
                     help="only the step (and e2e): skip allreduce/broadcast/NCCL/EASGD/config-4")
     ap.add_argument("--algo", type=int, default=0,
-                    help="0 auto, 1 two-shot pull, 3 two-shot push, 4 NVLS, 6 TMA, 7 balanced")
+                    help="0 auto, 1 register two-shot, 4 NVLS, 6 TMA two-shot")
     ap.add_argument("--switch", default="auto", choices=["auto", "on", "off"],
                     help="let the automatic choice use NVLS (tc_comm_set_switch_reduction): "
                          "auto = from N = 5, where it moves fewer bytes than the two-shot")

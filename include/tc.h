@@ -144,19 +144,16 @@ TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, in
  * (16 MiB / (16 p) elements).  Must be identical on all ranks.  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes);
 
-/* Large-group algorithm (must be identical on all ranks): 0 = automatic, 1 = two-shot with
- * pulled reduce-scatter (loads from peers' tensors), 3 = two-shot with pushed reduce-scatter
- * (stores into the owners' receive scratch), 4 = NVLS (switch reduction, multimem.ld_reduce +
- * multimem.st; only for groups in tc_mem_alloc memory, else two-shot).  1 and 3 end with the
- * staged pull allgather and give bit-identical results (float64, rank order).  NVLS sums in
- * the switch in fp32 (order unspecified): exact for integer-valued data, else within the
- * BASELINE tolerance 1e-5 * sum_k |x_k| of the float64 sum; identical on every rank.  6 =
- * two-shot pull with the data moved by TMA bulk copies through a shared-memory stage ring (one
- * CTA per SM at most; tc_comm_set_tuning's num_ctas sets how many SMs it occupies); 7 = the
- * same with tiles claimed from per-rank counters instead of dealt round-robin.  1, 3, 6 and 7
- * give bit-identical results.  Automatic (0): low-latency / one-shot for small groups, 6 above
- * (measured fastest); NVLS only when tc_comm_set_switch_reduction(comm, 1) allowed it.
- * Errors: TC_ERR_INVALID_ARG. */
+/* Large-group algorithm (must be identical on all ranks): 0 = automatic; 1 = two-shot with the
+ * reduce-scatter and allgather pulled by the SMs' 16-B loads (register kernels); 6 = two-shot
+ * with the data moved by TMA bulk copies through a shared-memory stage ring (one CTA per SM at
+ * most; tc_comm_set_tuning's num_ctas or tc_group_set_num_ctas sets how many SMs it occupies);
+ * 1 and 6 give bit-identical results (float64, rank order).  4 = NVLS (switch reduction,
+ * multimem.ld_reduce + multimem.st; only for groups in tc_mem_alloc memory, else two-shot): the
+ * switch sums in fp32 in its own order -- exact for integer-valued data, else within the
+ * BASELINE tolerance 1e-5 * sum_k |x_k| of the float64 sum; identical on every rank.
+ * Automatic (0): low-latency / one-shot for small groups, 6 above (measured fastest); NVLS only
+ * when tc_comm_set_switch_reduction(comm, 1) allowed it.  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_algorithm(tc_comm* comm, int algo);
 
 /* Whether the AUTOMATIC choice may use the NVSwitch reduction (algorithm 4) for groups in
@@ -323,9 +320,8 @@ TC_API tc_status tc_easgd_async_update(tc_group* x, tc_group* center, float alph
 TC_API tc_status tc_broadcast(tc_group* x, int root, void* stream);
 
 /* Introspection of the most recent hot-path launch on this comm (for benchmarks):
- * algorithm (0 = local p=1, 1 = two-shot pull, 2 = one-shot, 3 = two-shot push, 4 = NVLS,
- * 5 = low-latency, 6 = two-shot TMA, 7 = two-shot TMA with claimed tiles), grid CTAs per
- * rank, threads per CTA. */
+ * algorithm (0 = local p=1, 1 = two-shot (register), 2 = one-shot, 4 = NVLS, 5 = low-latency,
+ * 6 = two-shot TMA), grid CTAs per rank, threads per CTA. */
 TC_API tc_status tc_comm_last_launch(const tc_comm* comm, int* algo, int* ctas, int* threads);
 
 #ifdef __cplusplus

@@ -95,11 +95,11 @@ enum Algo {
   ALGO_LOCAL = 0,
   ALGO_TWOSHOT = 1,
   ALGO_ONESHOT = 2,
-  ALGO_TWOSHOT_PUSH = 3,
+  // 3 (register push two-shot) and 7 (TMA two-shot with claimed tiles): removed in round 2,
+  // measured never faster than 6
   ALGO_NVLS = 4,
   ALGO_LL = 5,
   ALGO_TWOSHOT_TMA = 6,
-  ALGO_TWOSHOT_BAL = 7
 };
 
 // ---------------------------------------------------------------- A1 descriptor (host)
@@ -133,8 +133,6 @@ tc_status bootstrap_allgather(tc_allgather_fn ag, void* ctx, int nranks, const v
 struct DevState {
   uint32_t epoch;
   uint32_t done;
-  uint32_t ctr_rs, ctr_ag;  // balanced TMA two-shot: next unclaimed tile of each phase
-  uint32_t done_rs;         // CTAs that finished the reduce-scatter
   uint32_t pad;
 };
 
@@ -161,7 +159,7 @@ struct KParams {
   uint32_t* const* flags;// [p] flag buffers (peer-mapped)
   float* const* stage;   // [p] one-shot staging (+ low-latency buffers), peer-mapped
   int ll_cap;            // low-latency elements per source per parity
-  float* const* arena;   // [p] per-rank arena: staging chunk x2 (parity) + p receive scratch
+  float* const* arena;   // [p] per-rank arena: staging chunk x2 (parity)
   int chunk_cap;         // slots per arena region (>= the largest owner chunk)
   DevState* state;       // [p] device-side call epochs (this process's ranks are valid)
   float scale, lr, mu, wd, rescale, alpha;

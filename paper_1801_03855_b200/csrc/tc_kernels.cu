@@ -32,7 +32,7 @@ struct Shape {
 Shape shape_of(int op, int algo, int p, int threads) {
   if (algo == ALGO_LOCAL)
     return {kTmaThreads, op == OP_ESGD ? kTmaSmem4 : kTmaSmem};
-  if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL) return {kT2Threads, t2_smem(op, p)};
+  if (algo == ALGO_TWOSHOT_TMA) return {kT2Threads, t2_smem(op, p)};
   if (algo == ALGO_NVLS) return {kNvlsThreads, 0};
   return {threads, 0};
 }

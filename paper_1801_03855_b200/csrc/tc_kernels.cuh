@@ -18,9 +18,6 @@
 //    barrier -> allgather: pull every other owner's staged chunk (rotated start), epilogue.
 //    No exit barrier: peers read only staging, which is rewritten two calls later, after the
 //    next call's first barrier proved every peer finished this one.
-//  * Two-shot, push: every rank first STORES its contribution to each owner's receive scratch
-//    (stores beat loads over NVLink), signalling per owner; the owner reduces from local HBM in
-//    the same canonical order, then the staged pull allgather as above.  No entry barrier.
 //  * One-shot (A5, small groups): copy the group into a parity-selected staging buffer, ENTRY
 //    barrier, every rank reduces all slots from all p staging buffers.
 //  * Local (p = 1): the epilogue as a single HBM stream.
@@ -115,7 +112,6 @@ __device__ __forceinline__ void call_end(const KParams& kp, int r) {
     DevState* st = kp.state + r;
     if (atomicAdd(&st->done, 1u) == gridDim.x - 1) {
       st->done = 0;
-      st->ctr_rs = st->ctr_ag = st->done_rs = 0;  // (balanced two-shot; every CTA is past them)
       __threadfence();
       *(volatile uint32_t*)&st->epoch = s_epoch;
     }
@@ -379,12 +375,9 @@ __device__ __forceinline__ void stv(float* base, const SlotRef& ref, float4 v) {
   }
 }
 
-// Staging / scratch regions of the per-rank arena (flat, slot-indexed relative to a chunk).
+// Staging regions of the per-rank arena (flat, slot-indexed relative to a chunk).
 __device__ __forceinline__ float* arena_stage(const KParams& kp, int rank, int parity) {
   return kp.arena[rank] + (size_t)parity * kp.chunk_cap * 4;
-}
-__device__ __forceinline__ float* arena_scratch(const KParams& kp, int rank, int src) {
-  return kp.arena[rank] + (size_t)(2 + src) * kp.chunk_cap * 4;
 }
 
 // [lo, hi) is cut into pieces of kPiece slots dealt round-robin to the CTAs of the grid (then
@@ -458,7 +451,6 @@ __device__ __forceinline__ void slot_loop_flat(const KParams& kp, int lo, int hi
 // ------------------------------------------------------------------ phase bodies
 enum SrcKind {
   SRC_TENSORS = 0,   // every rank's primary tensor (pull reduce-scatter, local path)
-  SRC_SCRATCH = 1,   // own primary tensor for k == r, else own receive scratch of rank k (push)
   SRC_ONESHOT = 2,   // every rank's one-shot staging buffer (flat over the whole group)
 };
 
@@ -471,7 +463,7 @@ struct ReduceBody {
   static constexpr int NP = 3 + (SRC == SRC_TENSORS ? P : 0);
   const KParams& kp;
   int r;
-  int origin;         // first slot of the chunk (flat offsets of staging / scratch)
+  int origin;         // first slot of the chunk (flat offset of staging)
   float* stage_out;   // this rank's staging chunk (STAGE_OUT)
   struct State {
     float4 x[P];
@@ -495,9 +487,6 @@ struct ReduceBody {
     for (int k = 0; k < P; ++k) {
       if constexpr (SRC == SRC_TENSORS) {
         st.x[k] = ldv<VEC>(ptr[3 + k], ref);
-      } else if constexpr (SRC == SRC_SCRATCH) {
-        st.x[k] = (k == r) ? ldv<VEC>(ptr[0], ref)
-                           : ld16(arena_scratch(kp, r, k) + (size_t)(ref.s - origin) * 4);
       } else {
         st.x[k] = ld16(kp.stage[k] + stage_off() + (size_t)ref.s * 4);
       }
@@ -582,8 +571,7 @@ struct GatherBody {
   }
 };
 
-// Copy this rank's primary tensors into a flat destination (push to an owner's scratch, or
-// the one-shot staging buffer).
+// Copy this rank's primary tensors into a flat destination (the one-shot staging buffer).
 struct CopyOutBody {
   static constexpr int NP = 1;
   const KParams& kp;
@@ -773,39 +761,6 @@ __global__ void __launch_bounds__(512, MINB) k_twoshot_pull(KParams kp) {
   const int lo = (int)(M * r / P), hi = (int)(M * (r + 1) / P);
   {
     ReduceBody<OP, P, SRC_TENSORS, true> body{kp, r, lo, arena_stage(kp, r, par)};
-    slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
-  }
-  stamp(kp, 2);
-  stamp(kp, 3);
-  if (!gather_all<OP, P, MINB>(kp, r, par)) return;
-  stamp(kp, 4);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
-
-template <int OP, int P, int MINB>
-__global__ void __launch_bounds__(512, MINB) k_twoshot_push(KParams kp) {
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  call_begin(kp, r);
-  const int par = (int)(ep() & 1u);
-  const int64_t M = kp.M;
-  stamp(kp, 0);
-  // push my contribution to this CTA's pieces of every other chunk into its owner's scratch
-#pragma unroll 1
-  for (int j = 1; j < P; ++j) {
-    const int q = (r + j) % P;
-    const int lo = (int)(M * q / P), hi = (int)(M * (q + 1) / P);
-    CopyOutBody body{kp, r, lo, arena_scratch(kp, q, r)};
-    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
-    __syncthreads();
-    if (threadIdx.x == 0) signal_one(kp, BAR_ENTRY, r, q);
-  }
-  stamp(kp, 1);
-  if (!barrier_all(kp, r, BAR_ENTRY, false)) return;  // every peer's push has landed
-  const int lo = (int)(M * r / P), hi = (int)(M * (r + 1) / P);
-  {
-    ReduceBody<OP, P, SRC_SCRATCH, true> body{kp, r, lo, arena_stage(kp, r, par)};
     slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
   }
   stamp(kp, 2);
@@ -1422,223 +1377,6 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_tma(KParams kp) {
   stamp(kp, 5);
 }
 
-// ------------------------------------------------------------------ two-shot, TMA, balanced
-// The TMA two-shot with tiles claimed from per-rank counters instead of dealt round-robin, so
-// CTAs on slower SMs take fewer tiles (the static deal waits for the slowest CTA of each pair:
-// MID barrier medians of 25-35 us).  Claims are kClaim tiles (one latency chain per claim; the
-// stage ring covers it).  Because any CTA may hold any tile, ENTRY is one arrival flag per rank
-// (written by CTA 0) and MID is per rank: the last CTA of a rank to finish its reduce-scatter
-// (a device-scope counter) signals every peer after a system fence; every CTA waits for all
-// peers' signals before the allgather.  Units carry their phase; a unit of zero tiles ends a
-// phase.
-constexpr int kClaim = 8;
-
-template <int OP, int P>
-__global__ void __launch_bounds__(kT2Threads, 1) k_twoshot_bal(KParams kp) {
-  using NR = Needs<OP, PH_RS, P>;
-  using NG = Needs<OP, PH_AG, 2>;
-  constexpr int OPS = t2_ops(OP, P), NS = t2_stages(OP, P);
-  constexpr int OPS_RS = P + NR::loadB + NR::loadC + NR::loadD;
-  constexpr int OPS_AG = 1 + NG::loadA + NG::loadB + NG::loadC + NG::loadD;
-  constexpr int G_RS = t2_pack(OPS / OPS_RS), G_AG = t2_pack(OPS / OPS_AG);
-  constexpr int V = t2_slots(P);
-  extern __shared__ __align__(128) float4 sm4[];  // [NS][OPS][V]
-  __shared__ __align__(8) uint64_t full[NS], empty[NS];
-  __shared__ T2Desc desc[NS][8];
-  __shared__ int unit_n[NS];
-  const int r = kp.rank0 + (int)blockIdx.y;
-  if (r == kp.absent_rank) return;
-  const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[s])),
-                   "r"(kT2ConsumerWarps));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  call_begin(kp, r);  // (its __syncthreads publishes the barrier init)
-  const uint32_t e = ep();
-  const int par = (int)(e & 1u);
-  stamp(kp, 0);
-  if (blockIdx.x == 0 && threadIdx.x < P && (int)threadIdx.x != r)
-    st_release_sys(kp.flags[threadIdx.x] + flag_index(BAR_ENTRY, r, 0), e);
-  const size_t T = (size_t)kp.T;
-  const int64_t M = kp.M;
-  DevState* st = kp.state + r;
-  auto stage = [&](int s, int o) { return sm4 + ((size_t)s * OPS + o) * V; };
-  auto wait_flags = [&](int bar) -> bool {  // lanes < P of the calling warp
-    bool ok = true;
-    if (lane_id < P && lane_id != r) {
-      const uint32_t* f = kp.flags[r] + flag_index(bar, lane_id, 0);
-      if ((int32_t)(ld_acquire_sys(f) - e) < 0) {
-        const unsigned long long t0 = globaltimer();
-        while ((int32_t)(ld_acquire_sys(f) - e) < 0)
-          if (globaltimer() - t0 > kp.timeout_ns) {
-            atomicCAS_system(kp.err, 0, (int)TC_ERR_TIMEOUT);
-            ok = false;
-            break;
-          }
-      }
-    }
-    return __all_sync(0xffffffffu, ok);
-  };
-  int k = 0;
-  bool ok = true;
-  // producer: one phase of claimed tiles, then a zero-tile unit
-  auto produce = [&](int ph) {
-    constexpr int GMAXP = G_RS > G_AG ? G_RS : G_AG;
-    const int G = ph == PH_RS ? G_RS : G_AG;
-    const int opsp = ph == PH_RS ? OPS_RS : OPS_AG;
-    uint32_t* ctr = ph == PH_RS ? &st->ctr_rs : &st->ctr_ag;
-    const int n_r = kp.tile2_off[r + 1] - kp.tile2_off[r];
-    const int total = ph == PH_RS ? n_r : kp.tile2_off[P] - n_r;
-    (void)GMAXP;
-    while (ok) {
-      int start = 0;
-      if (lane_id == 0) start = (int)atomicAdd(ctr, (uint32_t)kClaim);
-      start = __shfl_sync(0xffffffffu, start, 0);
-      if (start >= total) break;
-      const int j = start + lane_id;
-      const bool valid = lane_id < kClaim && j < total;
-      T2Desc d{};
-      const float* src[OPS];
-      if (valid) {
-        int qo = r, gi;
-        if (ph == PH_RS) {
-          gi = kp.tile2_off[r] + j;
-        } else {  // owners r+1, r+2, ... in turn
-          int rem = j;
-#pragma unroll 1
-          for (int jq = 1; jq < P; ++jq) {
-            qo = (r + jq) % P;
-            const int n_q = kp.tile2_off[qo + 1] - kp.tile2_off[qo];
-            if (rem < n_q) break;
-            rem -= n_q;
-          }
-          gi = kp.tile2_off[qo] + rem;
-        }
-        const int4 tl = kp.tiles2[gi];
-        d.t = tl.x;
-        d.n = tl.z;
-        d.e = (int64_t)(tl.y - kp.prefix[d.t]) * 4 - kp.shift[d.t];
-        const size_t mine = (size_t)r * T + d.t;
-        d.a = kp.a[mine] + d.e;
-        d.b = kp.b != nullptr ? kp.b[mine] + d.e : nullptr;
-        d.c = kp.c != nullptr ? kp.c[mine] + d.e : nullptr;
-        d.g = kp.d != nullptr ? kp.d[mine] + d.e : nullptr;
-        d.st = arena_stage(kp, qo, par) + (size_t)(tl.y - (int)(M * qo / P)) * 4;
-        const bool part = d.e < 0 || d.e + 4 * (int64_t)d.n > kp.numel[d.t];
-        bool vec = (!part || d.n == 1) && ((uintptr_t)d.a & 15) == 0;
-        int o = 0;
-        if (ph == PH_RS) {
-#pragma unroll
-          for (int q = 0; q < P; ++q) src[o++] = kp.a[q * T + d.t] + d.e;
-          if (NR::loadB) src[o++] = d.b;
-          if (NR::loadC) src[o++] = d.c;
-          if (NR::loadD) src[o++] = d.g;
-        } else {
-          src[o++] = d.st;
-          if (NG::loadA) src[o++] = d.a;
-          if (NG::loadB) src[o++] = d.b;
-          if (NG::loadC) src[o++] = d.c;
-          if (NG::loadD) src[o++] = d.g;
-        }
-        for (int x = 0; x < o; ++x) vec = vec && (((uintptr_t)src[x] & 15) == 0);
-        d.vec = vec ? (part ? 2 : 1) : 0;
-      }
-      const int nclaim = min(kClaim, total - start);
-      for (int u0 = 0; u0 < nclaim; u0 += G) {
-        const int s = k % NS;
-        const bool in_unit = valid && lane_id >= u0 && lane_id < u0 + G;
-        const uint32_t ub = __reduce_add_sync(
-            0xffffffffu, (in_unit && d.vec) ? (uint32_t)d.n * 16 * opsp : 0u);
-        if (lane_id == 0 && k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS - 1) & 1));
-        __syncwarp();
-        if (in_unit) desc[s][lane_id - u0] = d;
-        if (lane_id == 0) unit_n[s] = min(G, nclaim - u0);
-        __syncwarp();
-        if (lane_id == 0) {
-          if (ub)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                             smem_u32(&full[s])), "r"(ub) : "memory");
-          else
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s]))
-                         : "memory");
-        }
-        __syncwarp();
-        if (in_unit && d.vec)
-          for (int x = 0; x < opsp; ++x)
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-                "%2, [%3];" ::"r"(smem_u32(stage(s, (lane_id - u0) * opsp + x))),
-                "l"(src[x]), "r"((uint32_t)d.n * 16), "r"(smem_u32(&full[s]))
-                : "memory");
-        ++k;
-      }
-    }
-    const int s = k % NS;  // end of the phase
-    if (lane_id == 0) {
-      if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS - 1) & 1));
-      unit_n[s] = 0;
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s]))
-                   : "memory");
-    }
-    __syncwarp();
-    ++k;
-  };
-  auto consume = [&](int ph) {
-    const int ct = threadIdx.x - 32, nct = kT2Threads - 32;
-    while (true) {
-      const int s = k % NS;
-      mbar_wait(&full[s], (uint32_t)((k / NS) & 1));
-      const int n = unit_n[s];
-      for (int jt = 0; jt < n; ++jt) {
-        if (ph == PH_RS)
-          t2_tile<OP, P, PH_RS, OPS_RS, V>(kp, r, desc[s][jt], stage(s, jt * OPS_RS), ct, nct);
-        else
-          t2_tile<OP, P, PH_AG, OPS_AG, V>(kp, r, desc[s][jt], stage(s, jt * OPS_AG), ct, nct);
-      }
-      __syncwarp();
-      if (lane_id == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
-                     : "memory");
-      ++k;
-      if (n == 0) break;
-    }
-  };
-  if (warp == 0) {
-    ok = wait_flags(BAR_ENTRY);
-    if (lane_id == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncwarp();
-    produce(PH_RS);
-  } else {
-    consume(PH_RS);
-  }
-  stamp(kp, 2);
-  // MID, per rank: the last CTA of this rank to finish its reduce-scatter signals every peer
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&st->done_rs, 1u) == gridDim.x - 1) {
-      __threadfence_system();
-      for (int q = 0; q < P; ++q)
-        if (q != r) st_release_sys(kp.flags[q] + flag_index(BAR_MID, r, 0), e);
-    }
-  }
-  if (warp == 0) {
-    ok = ok && wait_flags(BAR_MID);
-    if (lane_id == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncwarp();
-  }
-  __syncthreads();
-  stamp(kp, 3);
-  if (warp == 0) produce(PH_AG);
-  else consume(PH_AG);
-  stamp(kp, 4);
-  call_end(kp, r);
-  stamp(kp, 5);
-}
 
 // ------------------------------------------------------------------ NVLS (switch reduction)
 // The owner of a chunk reads every rank's copy of it reduced in the NVSwitch
@@ -1987,11 +1725,9 @@ const void* kernel_ptr(int algo, int p) {
       if (algo == ALGO_NVLS) return (const void*)k_nvls<OP, PP>;                             \
     if (algo == ALGO_NVLS) return nullptr;                                                   \
     if (algo == ALGO_TWOSHOT_TMA) return (const void*)k_twoshot_tma<OP, PP>;                 \
-    if (algo == ALGO_TWOSHOT_BAL) return (const void*)k_twoshot_bal<OP, PP>;                 \
     if (algo == ALGO_LL) return (const void*)k_ll<OP, PP, 2>;                                \
-    return algo == ALGO_TWOSHOT        ? (const void*)k_twoshot_pull<OP, PP, 2>              \
-           : algo == ALGO_TWOSHOT_PUSH ? (const void*)k_twoshot_push<OP, PP, 2>              \
-                                       : (const void*)k_oneshot<OP, PP, 2>;
+    return algo == ALGO_TWOSHOT ? (const void*)k_twoshot_pull<OP, PP, 2>                     \
+                                : (const void*)k_oneshot<OP, PP, 2>;
   switch (p) {
     TC_CASE(2) TC_CASE(3) TC_CASE(4) TC_CASE(5) TC_CASE(6) TC_CASE(7) TC_CASE(8)
     default: return nullptr;

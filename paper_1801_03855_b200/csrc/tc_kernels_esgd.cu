@@ -6,18 +6,6 @@
 namespace tc {
 const void* kernel_ptr_esgd(int algo, int p) {
   if (algo == ALGO_LOCAL) return (const void*)k_local_tma<OP_ESGD>;
-  if (algo == ALGO_TWOSHOT_BAL) {
-    switch (p) {
-      case 2: return (const void*)k_twoshot_bal<OP_ESGD, 2>;
-      case 3: return (const void*)k_twoshot_bal<OP_ESGD, 3>;
-      case 4: return (const void*)k_twoshot_bal<OP_ESGD, 4>;
-      case 5: return (const void*)k_twoshot_bal<OP_ESGD, 5>;
-      case 6: return (const void*)k_twoshot_bal<OP_ESGD, 6>;
-      case 7: return (const void*)k_twoshot_bal<OP_ESGD, 7>;
-      case 8: return (const void*)k_twoshot_bal<OP_ESGD, 8>;
-    }
-    return nullptr;
-  }
   if (algo != ALGO_TWOSHOT_TMA) return nullptr;
   switch (p) {
     case 2: return (const void*)k_twoshot_tma<OP_ESGD, 2>;

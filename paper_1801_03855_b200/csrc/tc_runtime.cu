@@ -292,14 +292,14 @@ tc_status upload_group(Group& g, const std::vector<uint8_t>& vec_ok) {
 
 bool finite(float v) { return std::isfinite(v); }
 
-// Grow the per-rank arena (staging chunk x2 + p receive scratch regions of `cap` slots each) to
+// Grow the per-rank arena (two parity-selected staging chunks of `cap` slots each) to
 // hold owner chunks of `need` slots.  Collective (called from tc_group_create on every rank).
 tc_status grow_arena(Comm& c, int64_t need) {
   const int p = c.nranks;
   if (p == 1 || need <= c.arena_cap) return TC_OK;
   int64_t cap = std::max<int64_t>(need, (int64_t)1 << 16);
   cap = (cap + 4095) & ~(int64_t)4095;
-  const size_t bytes = (size_t)(2 + p) * (size_t)cap * 16;
+  const size_t bytes = (size_t)2 * (size_t)cap * 16;
   TC_CUDA(cudaDeviceSynchronize());
   tc_status st = comm_barrier(c);  // no kernel on any rank still uses the old arenas
   if (st != TC_OK) return st;
@@ -413,7 +413,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     algo = ALGO_TWOSHOT_TMA;
     if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   } else if (op == OP_ESGD) {
-    algo = c.algo_override == ALGO_TWOSHOT_BAL ? ALGO_TWOSHOT_BAL : ALGO_TWOSHOT_TMA;
+    algo = ALGO_TWOSHOT_TMA;
     if ((Mdev + p - 1) / p + 1 > c.arena_cap) return TC_ERR_CUDA;
   } else {
     // One-shot moves (p-1)S per GPU against 2(p-1)/p S for two-shot but needs one barrier
@@ -446,9 +446,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     const int64_t ll_lim = c.tune_ll < 0 ? ll_auto : c.tune_ll;
     if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
     else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;
-    else if (c.algo_override == ALGO_TWOSHOT_PUSH) algo = ALGO_TWOSHOT_PUSH;
     else if (c.algo_override == ALGO_TWOSHOT_TMA) algo = ALGO_TWOSHOT_TMA;
-    else if (c.algo_override == ALGO_TWOSHOT_BAL) algo = ALGO_TWOSHOT_BAL;
     else if (c.algo_override == ALGO_TWOSHOT) algo = ALGO_TWOSHOT;
     else if (nvls_ok && (c.algo_override == ALGO_NVLS ||
                          (c.algo_override == 0 && c.allow_switch && p >= 5)))
@@ -456,8 +454,7 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     // TMA-staged two-shot: ResNet-50 group p = 2 allreduce 188 / SGD step 197 us (LDG pull
     // 208 / 226, NCCL allreduce 219); p = 4 262 / 278 us (pull 289 / 301, NCCL 274-276).
     else algo = ALGO_TWOSHOT_TMA;
-    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH || algo == ALGO_TWOSHOT_TMA ||
-         algo == ALGO_TWOSHOT_BAL) &&
+    if ((algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_TMA) &&
         (Mdev + p - 1) / p + 1 > c.arena_cap)
       return TC_ERR_CUDA;
   }
@@ -466,11 +463,11 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
   if (occ < 1) return TC_ERR_CUDA;
   int cap = c.num_sms * occ / nlocal;  // co-resident CTAs per rank
   if (cap < 1) cap = 1;
-  const bool twoshot = algo == ALGO_TWOSHOT || algo == ALGO_TWOSHOT_PUSH;
+  const bool twoshot = algo == ALGO_TWOSHOT;
   int64_t work_slots = twoshot ? (Mdev + p - 1) / p : Mdev;
   int64_t want = (work_slots + threads - 1) / threads;
   int ctas;
-  if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_TWOSHOT_BAL || algo == ALGO_NVLS) {
+  if (algo == ALGO_TWOSHOT_TMA || algo == ALGO_NVLS) {
     // bytes in flight come from the stage ring, not from threads: one CTA per SM at most
     // (NVLS walks its own table of smaller tiles)
     const std::vector<int>& off = algo == ALGO_NVLS ? ga->tile_nv_off : ga->tile2_off;
@@ -639,8 +636,8 @@ tc_status tc_comm_set_ll_max(tc_comm* comm, int64_t bytes) {
 }
 
 tc_status tc_comm_set_algorithm(tc_comm* comm, int algo) {
-  if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_TWOSHOT_PUSH &&
-                algo != ALGO_NVLS && algo != ALGO_TWOSHOT_TMA && algo != ALGO_TWOSHOT_BAL))
+  if (!comm || (algo != 0 && algo != ALGO_TWOSHOT && algo != ALGO_NVLS &&
+                algo != ALGO_TWOSHOT_TMA))
     return TC_ERR_INVALID_ARG;
   comm->c.algo_override = algo;
   return TC_OK;

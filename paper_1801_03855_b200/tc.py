@@ -27,9 +27,8 @@ STATUS = {
 }
 TC_OK, TC_ERR_INVALID_ARG, TC_ERR_SHAPE_MISMATCH, TC_ERR_NOT_SHAREABLE = 0, 1, 2, 3
 TC_ERR_BUSY, TC_ERR_TIMEOUT, TC_ERR_CUDA, TC_ERR_BOOTSTRAP, TC_ERR_UNSUPPORTED = 4, 5, 6, 7, 8
-ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 3: "two-shot-push", 4: "nvls", 5: "ll",
-              6: "two-shot-tma", 7: "two-shot-bal"}
-ALGO_AUTO, ALGO_TWOSHOT_PULL, ALGO_TWOSHOT_PUSH, ALGO_NVLS, ALGO_TWOSHOT_TMA = 0, 1, 3, 4, 6
+ALGO_NAMES = {0: "local", 1: "two-shot", 2: "one-shot", 4: "nvls", 5: "ll", 6: "two-shot-tma"}
+ALGO_AUTO, ALGO_TWOSHOT_PULL, ALGO_NVLS, ALGO_TWOSHOT_TMA = 0, 1, 4, 6
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_size_t)
@@ -280,7 +279,7 @@ class Comm:
         self._sym = [t for t in getattr(self, "_sym", []) if t is not tensor]
 
     def set_algorithm(self, algo: int):
-        """0 = automatic, 1 = two-shot pull, 3 = two-shot push (identical results),
+        """0 = automatic, 1 = register two-shot, 6 = TMA two-shot (identical results),
         4 = NVLS for groups in symmetric memory."""
         _check(LIB.tc_comm_set_algorithm(self.h, int(algo)), "set_algorithm")
 

@@ -32,7 +32,7 @@ def main():
     cases = [(W.TINY, "int", 0), (W.TINY, "int", 1 << 20),
              ([7, 13, 1000, 0, 50001, 3, 262144], "grad", 0),
              ([7, 13, 1000, 0, 5001, 3], "grad", 1 << 20)]
-    for (numels, kind, oneshot), algo in [(c, a) for c in cases for a in (1, 3, 5, 6, 7)]:
+    for (numels, kind, oneshot), algo in [(c, a) for c in cases for a in (1, 5, 6)]:
         comm.set_tuning(0, 0, oneshot)
         comm.set_ll_max(1 << 30 if algo == 5 else 0)
         comm.set_algorithm(algo if algo != 5 else 0)
@@ -44,7 +44,7 @@ def main():
         assert comm.async_error() == 0
 
     # SGD (fused) and EASGD, two-shot and one-shot
-    for oneshot, algo in ((0, 1), (0, 3), (1 << 20, 0), (0, 5), (0, 6), (0, 7)):
+    for oneshot, algo in ((0, 1), (1 << 20, 0), (0, 5), (0, 6)):
         comm.set_tuning(0, 0, oneshot)
         comm.set_ll_max(1 << 30 if algo == 5 else 0)
         comm.set_algorithm(algo if algo != 5 else 0)
@@ -127,7 +127,7 @@ def main():
     numels = [7, 13, 1000, 0, 50001, 3, 262144]
     sym = comm.alloc_symmetric(sum(numels) + 64)
     views = list(torch.split(sym[:sum(numels)], numels))
-    algos = [1, 3, 6, 7] + ([4] if comm.multicast_supported else [])
+    algos = [1, 6] + ([4] if comm.multicast_supported else [])
     comm.set_tuning(0, 0, 0)
     comm.set_ll_max(0)
     with tc.Group(comm, views) as g:

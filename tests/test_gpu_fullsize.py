@@ -11,8 +11,8 @@ Covered (BASELINE.json configs):
       p = 1: the TMA stream (k_local_tma) with allreduce scale != 1, the fused SGD step, the
              elastic update and the fused elastic + SGD step; 12.5k tiles, so the 4-stage ring
              wraps thousands of times;
-      p = 2, 4, 8: TMA two-shot (algorithm 6, the bench default) and the balanced variant (7)
-             for allreduce, fused SGD, EASGD and fused elastic + SGD.
+      p = 2, 4, 8: TMA two-shot (algorithm 6, the bench default) for allreduce, fused SGD, EASGD
+             and fused elastic + SGD, and the register two-shot (algorithm 1) for the first three.
   * config 3 -- AlexNet (61.1 M) and VGG-16 (138.4 M) at p = 1, 2, 4 (default algorithm).
   * config 4 -- 2 clients x 4 ranks on the ResNet-50 parameters, 16 steps, tau = 4.
   * config 5 -- 4 / 16 / 64 / 256 MiB (the paper's 4/16/64 MB sizes, plus 256 MiB)
@@ -38,7 +38,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 SGD_HP = dict(lr=0.1, momentum=0.9, wd=1e-4)
 ALPHA = 0.1
-ALGO = {"tma": 6, "bal": 7, "auto": 0}
+ALGO = {"tma": 6, "pull": 1, "auto": 0}
 
 
 @functools.lru_cache(maxsize=24)
@@ -76,7 +76,7 @@ def _pick(p):
 
 
 def _want_algo(p, algo):
-    return "local" if p == 1 else ("two-shot-bal" if algo == "bal" else "two-shot-tma")
+    return "local" if p == 1 else ("two-shot" if algo == "pull" else "two-shot-tma")
 
 
 def _check_allreduce(name, p, algo, cfg, scale=0.37):
@@ -181,11 +181,14 @@ def test_resnet50_p1_tma_stream(op):
     assert OPS[op]("resnet50", 1, "auto") == "local"
 
 
-@pytest.mark.parametrize("algo", ["tma", "bal"])
+@pytest.mark.parametrize("algo", ["tma", "pull"])
 @pytest.mark.parametrize("op", sorted(OPS))
 @pytest.mark.parametrize("p", [2, 4, 8])
 def test_resnet50_twoshot(p, op, algo):
-    """bench.py N >= 2 default (algorithm 6, TMA two-shot) and the balanced variant (7)."""
+    """bench.py N >= 2 default (algorithm 6, TMA two-shot) and the register two-shot (1), an
+    independent implementation of the same arithmetic (ESGD exists in the TMA kernels only)."""
+    if op == "esgd" and algo == "pull":
+        pytest.skip("the fused elastic + SGD step is implemented by the TMA kernels only")
     assert OPS[op]("resnet50", p, algo) == _want_algo(p, algo)
 
 

@@ -25,12 +25,9 @@ pytestmark = pytest.mark.gpu
 
 ONESHOT = 1 << 20   # force one-shot
 TWOSHOT = 0         # force two-shot (pull reduce-scatter)
-PUSH = -2           # force two-shot with pushed reduce-scatter
 LL = -3             # force the low-latency algorithm
 TMA = -4            # force the TMA-staged two-shot
-BAL = -5            # force the TMA two-shot with claimed (balanced) tiles
-ALGOS = [("two-shot", TWOSHOT), ("two-shot-push", PUSH), ("one-shot", ONESHOT), ("ll", LL),
-         ("two-shot-tma", TMA), ("two-shot-bal", BAL)]
+ALGOS = [("two-shot", TWOSHOT), ("one-shot", ONESHOT), ("ll", LL), ("two-shot-tma", TMA)]
 
 
 def _comm(p, oneshot=-1, ctas=0):
@@ -40,14 +37,8 @@ def _comm(p, oneshot=-1, ctas=0):
         return c
     if oneshot != -1:
         c.set_ll_max(0)
-    if oneshot == PUSH:
-        c.set_algorithm(3)
-        oneshot = 0
-    elif oneshot == TMA:
+    if oneshot == TMA:
         c.set_algorithm(6)
-        oneshot = 0
-    elif oneshot == BAL:
-        c.set_algorithm(7)
         oneshot = 0
     elif oneshot == TWOSHOT and p > 1:
         c.set_algorithm(1)
@@ -111,7 +102,7 @@ def test_unaligned_tensors(p, offset):
     numels = [7, 13, 1000, 4096, 3, 1, 2]
     xs = [W.group(numels, "int", 76, 0, k, W.GRAD) for k in range(p)]
     off = (lambda k: k % 4) if offset == "per-rank" else offset
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL):
+    for oneshot in (TWOSHOT, ONESHOT, LL, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot, offset=off)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -150,7 +141,7 @@ def test_fewer_slots_than_ranks(p):
     """N < p: some owners have empty chunks."""
     numels = [1, 2] if p == 4 else [3, 0, 1]
     xs = [W.group(numels, "int", 75, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, TMA, BAL):
+    for oneshot in (TWOSHOT, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -161,7 +152,7 @@ def test_many_tensors_1024():
     g = np.random.default_rng(5)
     numels = W.random_numels(g, 1024, 700)
     xs = [W.group(numels, "grad", 74, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, ONESHOT, LL, TMA, BAL):
+    for oneshot in (TWOSHOT, ONESHOT, LL, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -173,7 +164,7 @@ def test_cta_counts(ctas):
     p = 3
     numels = [7, 13, 1000, 50000, 9]
     xs = [W.group(numels, "grad", 73, 0, k, W.GRAD) for k in range(p)]
-    for oneshot in (TWOSHOT, PUSH, TMA, BAL):
+    for oneshot in (TWOSHOT, TMA):
         out, _ = run_allreduce(xs, oneshot=oneshot, ctas=ctas)
         for r in range(p):
             assert_bitwise(out[r], O.allreduce(xs), f"rank {r}")
@@ -210,7 +201,7 @@ def test_repeated_calls_epochs():
     grp = tc.Group(comm, dev)
     want = O.allreduce(xs, 0.5)
     for i in range(60):
-        comm.set_algorithm((1, 3, 6, 7)[i % 4])
+        comm.set_algorithm((1, 6)[i % 2])
         comm.set_tuning(0, 0, ONESHOT if i % 3 == 0 else TWOSHOT)
         comm.set_ll_max(1 << 30 if i % 5 == 0 else 0)
         tc.allreduce(grp, 0.5)
@@ -224,7 +215,7 @@ def test_repeated_calls_epochs():
 
 def test_repeated_sgd_steps_fresh_gradients():
     """Eight consecutive fused SGD steps on one comm, a fresh gradient every step and the
-    algorithm rotating (pull, push, TMA, balanced TMA, one-shot, LL): w and dw carry every step
+    algorithm rotating (register pull, TMA two-shot, one-shot, LL): w and dw carry every step
     into the next, so a skipped or repeated call fails."""
     p = 4
     numels = [7, 13, 1000, 4096, 65, 20000]
@@ -235,7 +226,7 @@ def test_repeated_sgd_steps_fresh_gradients():
     dg = [to_dev(W.group(numels, "zeros", 0, 0, 0, 0)) for _ in range(p)]
     dwt, ddw = [to_dev(w) for _ in range(p)], [to_dev(dw) for _ in range(p)]
     G, Wg, D = tc.Group(comm, dg), tc.Group(comm, dwt), tc.Group(comm, ddw)
-    shapes = [(1, 0, 0), (3, 0, 0), (6, 0, 0), (7, 0, 0), (0, ONESHOT, 0), (0, 0, 1 << 30)]
+    shapes = [(1, 0, 0), (6, 0, 0), (0, ONESHOT, 0), (0, 0, 1 << 30)]
     for step in range(8):
         gs = [W.group(numels, "grad", 78, 10 + step, k, W.GRAD) for k in range(p)]
         for k in range(p):
@@ -301,7 +292,7 @@ def test_sgd_step(name, oneshot, hp):
 def test_sgd_tolerance_vs_f64():
     p = 8
     numels = [5000, 3, 77]
-    res, _, _, (gs, w, dw, rescale) = run_sgd(p, numels, "grad", SGD_PERF, PUSH)
+    res, _, _, (gs, w, dw, rescale) = run_sgd(p, numels, "grad", SGD_PERF, TWOSHOT)
     _, wr, dwr = O.sgd_step_f64([w] * p, gs, [dw] * p, rescale=rescale, **SGD_PERF)
     for t in range(len(numels)):
         sabs = sum(np.abs(gs[k][t].astype(np.float64)) for k in range(p))
@@ -376,7 +367,7 @@ def test_tiny_config_easgd_int_conservation():
     for i in range(c):
         assert_bitwise(res[i][0], wx[i])
         assert_bitwise(res[i][1], wc)
-    res, xs, center, _ = run_easgd(c, W.TINY, 0.5, kind="int", oneshot=PUSH)
+    res, xs, center, _ = run_easgd(c, W.TINY, 0.5, kind="int", oneshot=TMA)
     for t in range(3):
         before = sum(xs[i][t].astype(np.float64) for i in range(c)) + center[t]
         after = sum(res[i][0][t].astype(np.float64) for i in range(c)) + res[0][1][t]
@@ -414,7 +405,7 @@ def test_timeout_when_a_rank_is_absent():
     xs = [to_dev([np.ones(4096, np.float32)]) for _ in range(2)]
     grp = tc.Group(comm, xs)
     comm.set_tuning(0, 0, TWOSHOT)
-    comm.set_algorithm(3)
+    comm.set_algorithm(1)
     tc.allreduce(grp)
     torch.cuda.synchronize()
     assert comm.async_error() == tc.tc.TC_ERR_TIMEOUT
@@ -437,7 +428,7 @@ def test_config5_sweep_shapes(p, T):
         if not numels:
             continue
         xs = [W.group(numels, "grad", W.CFG_SWEEP, 0, k, W.GRAD) for k in range(p)]
-        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL, TMA, BAL)):
+        for oneshot in ((TWOSHOT,) if p == 1 else (TWOSHOT, ONESHOT, LL, TMA)):
             if oneshot == LL and total > (64 << 10):
                 continue
             comm = _comm(p, oneshot)
@@ -455,8 +446,7 @@ def test_config5_sweep_shapes(p, T):
 # ------------------------------------------------------------------ NEXT row f2: fused elastic + SGD
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("offset", [0, 1])
-@pytest.mark.parametrize("bal", [False, True])
-def test_esgd_step(p, offset, bal):
+def test_esgd_step(p, offset):
     """tc_esgd_step (one GPU per client) bit-exact vs oracle.esgd_step: ragged groups with
     multi-tile tensors; offset 1 shifts every tensor off its 16-B boundary (element path at
     p = 1 heads, shifted grid at p >= 2)."""
@@ -467,8 +457,6 @@ def test_esgd_step(p, offset, bal):
     dws = [W.group(numels, "dw", W.CFG_EASGD, 7, i, W.DW) for i in range(p)]
     hp = dict(alpha=0.1, lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / 128)
     comm = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
-    if bal:
-        comm.set_algorithm(7)
     dx = [to_dev(x, offset=offset) for x in xs]
     dc = [to_dev(center, offset=offset) for _ in range(p)]
     dg = [to_dev(g, offset=offset) for g in gs]
@@ -476,8 +464,7 @@ def test_esgd_step(p, offset, bal):
     pick = (lambda v: v) if p > 1 else (lambda v: v[0])
     X, C, G, D = (tc.Group(comm, pick(v)) for v in (dx, dc, dg, dd))
     tc.esgd_step(X, C, G, D, **hp)
-    assert comm.last_launch()[0] == ("local" if p == 1 else
-                                     "two-shot-bal" if bal else "two-shot-tma")
+    assert comm.last_launch()[0] == ("local" if p == 1 else "two-shot-tma")
     assert comm.async_error() == 0
     wx, wc, wd = O.esgd_step(xs, center, gs, dws, **hp)
     for i in range(p):

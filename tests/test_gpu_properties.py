@@ -15,8 +15,8 @@ from gpu_util import to_dev, to_host, assert_bitwise  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 # (algorithm id for set_algorithm, one-shot limit, LL limit)
-ALGOS = {"auto": (0, -1, -1), "pull": (1, 0, 0), "push": (3, 0, 0), "tma": (6, 0, 0),
-         "bal": (7, 0, 0), "oneshot": (0, 1 << 30, 0), "ll": (0, 0, 1 << 30)}
+ALGOS = {"auto": (0, -1, -1), "pull": (1, 0, 0), "tma": (6, 0, 0),
+         "oneshot": (0, 1 << 30, 0), "ll": (0, 0, 1 << 30)}
 
 
 @settings(max_examples=60, deadline=None)

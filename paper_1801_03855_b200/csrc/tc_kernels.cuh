@@ -1424,9 +1424,6 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #ifndef TC_NV_RW_SGD
 #define TC_NV_RW_SGD 4  // switch-reduction warps per CTA, fused SGD (the rest: signal + epilogue)
 #endif
-#ifndef TC_NV_BC_U
-#define TC_NV_BC_U 4    // switch broadcast: 16-B multicast stores in flight per lane
-#endif
 #ifndef TC_NV_RED_U_SGD
 #define TC_NV_RED_U_SGD 4  // fused SGD: switch reductions in flight per lane
 #endif
@@ -1683,7 +1680,7 @@ __global__ void __launch_bounds__(kNvlsThreads, 1) k_nvls_bcast(KParams kp) {
       const float* src = kp.a[row + d.t] + d.e;
       float* mc = kp.mc[d.t] + d.e;
       if (d.full && ((((uintptr_t)src | (uintptr_t)mc) & 15) == 0)) {
-        constexpr int U = TC_NV_BC_U;
+        constexpr int U = 4;  // (8 and 16 in flight: same 220 us at p = 4 -- the switch's rate)
         for (int s0 = lane_id; s0 < d.n; s0 += 32 * U) {
           float4 v[U];
 #pragma unroll

@@ -1,0 +1,154 @@
+#!/usr/bin/env python
+"""NEXT row f1 on a real backward pass: data-parallel ResNet-50 training steps whose gradient
+allreduce + SGD-momentum update (libtc) overlaps the backward computation bucket by bucket.
+
+    torchrun --nproc-per-node N bench_train.py [--batch 64] [--iters 20] [--bucket-mb 25]
+
+PAPER.md:59: gradients "are obtained as soon as a backward step for a layer is computed, these can
+be aggregated in parallel with the backward phase".  The model is torchvision's ResNet-50 (random
+init, synthetic 224x224 images and labels; bf16 autocast, fp32 master weights and gradients).
+Its 161 parameters are views of one flat weight buffer and its gradients views of one flat
+gradient buffer, so libtc groups wrap the model's own tensors (no copies):
+  serial   -- forward + backward, then one tc_sgd_step over the whole group;
+  overlap  -- tc.BucketedStep: a post-accumulate-grad hook on every parameter reports its
+              gradient ready; each bucket's fused allreduce + SGD launches on a side stream as
+              soon as its last gradient lands (backward order), while the backward continues;
+  compute  -- forward + backward alone (no step), the floor.
+Per-iteration device time (CUDA events, max over ranks); hidden fraction = (serial - overlap) /
+(serial - compute).  After the timed iterations every rank's weights are compared (bitwise hash
+allgather): the fused step keeps the replicas identical.  Rank 0 prints one JSON line per mode.
+"""
+import argparse
+import hashlib
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+import paper_1801_03855_b200 as tc  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--bucket-mb", type=float, default=25.0)
+    ap.add_argument("--ctas", type=int, default=0, help="CTA budget of the bucket launches")
+    a = ap.parse_args()
+    import torchvision
+
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.manual_seed(1234)  # same initial weights on every rank
+    model = torchvision.models.resnet50().cuda()
+    params = list(model.parameters())
+    numels = [p.numel() for p in params]
+    N = sum(numels)
+    # the weights and gradients as views of flat buffers (the layout libtc and DDP buckets use)
+    w_flat = torch.empty(N, device="cuda")
+    g_flat = torch.zeros(N, device="cuda")
+    d_flat = torch.zeros(N, device="cuda")
+    off = 0
+    for p in params:
+        n = p.numel()
+        w_flat[off:off + n].copy_(p.data.reshape(-1))
+        p.data = w_flat[off:off + n].view_as(p)
+        p.grad = g_flat[off:off + n].view_as(p)
+        off += n
+    wv = [p.data.view(-1) for p in params]
+    gv = [p.grad.view(-1) for p in params]
+    dv = list(torch.split(d_flat, numels))
+    comm = tc.Comm.single(local) if world == 1 else tc.Comm.from_process_group(device=local)
+    W, G, D = tc.Group(comm, wv), tc.Group(comm, gv), tc.Group(comm, dv)
+    hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (world * a.batch))
+    step = tc.BucketedStep(comm, gv, wv, dv, bucket_bytes=int(a.bucket_mb * (1 << 20)),
+                           ctas=a.ctas)
+    index = {id(p): t for t, p in enumerate(params)}
+    mode = {"hooks": False}
+
+    def hook(p):
+        if mode["hooks"]:
+            step.grad_ready(index[id(p)], **hp)
+
+    for p in params:
+        p.register_post_accumulate_grad_hook(hook)
+    x = torch.randn(a.batch, 3, 224, 224, device="cuda")
+    y = torch.randint(0, 1000, (a.batch,), device="cuda")
+    crit = torch.nn.CrossEntropyLoss()
+
+    def fwd_bwd():
+        g_flat.zero_()
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = crit(model(x), y)
+        loss.backward()
+
+    def it_compute():
+        fwd_bwd()
+
+    def it_serial():
+        fwd_bwd()
+        tc.sgd_step(W, G, D, **hp)
+
+    def it_overlap():
+        mode["hooks"] = True
+        fwd_bwd()
+        step.finish()
+        mode["hooks"] = False
+
+    def timed(fn):
+        for _ in range(a.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / a.iters * 1e3], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    t_compute = timed(it_compute)
+    t_serial = timed(it_serial)
+    t_overlap = timed(it_overlap)
+    t_step = timed(lambda: tc.sgd_step(W, G, D, **hp))
+    # replicas identical after every mode (the fused step applies the same G everywhere)
+    dig = hashlib.sha256(w_flat.cpu().numpy().tobytes()).digest()
+    h = torch.tensor([int.from_bytes(dig[:7], "little")], device="cuda")
+    same = True
+    if world > 1:
+        hs = [torch.zeros_like(h) for _ in range(world)]
+        dist.all_gather(hs, h)
+        same = all(int(v) == int(hs[0]) for v in hs)
+    if rank == 0:
+        print(json.dumps({
+            "bench": "resnet50 training step, f1 overlap (PAPER.md:59)", "n_gpus": world,
+            "batch_per_gpu": a.batch, "bucket_mb": a.bucket_mb, "buckets": step.nbuckets,
+            "ctas": a.ctas or "auto", "t_compute_us": t_compute, "t_serial_us": t_serial,
+            "t_overlap_us": t_overlap, "t_step_alone_us": t_step,
+            "hidden_fraction": (t_serial - t_overlap) / max(t_serial - t_compute, 1e-9),
+            "speedup_vs_serial": t_serial / t_overlap, "replicas_identical": same,
+            "data": "synthetic images/labels, random-init torchvision ResNet-50, bf16 autocast"}),
+            flush=True)
+    step.destroy()
+    for grp in (W, G, D):
+        grp.destroy()
+    comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -491,12 +491,25 @@ class BucketedStep:
     def grad_ready(self, t, compute_stream=None, **hp):
         """Tensor t's gradient has been written (on compute_stream).  Launches its bucket's
         collective when it was the bucket's last tensor."""
-        import torch
-        self.hp = hp
         b = self.bucket_of[t]
         self.missing[b] -= 1
         if self.missing[b]:
+            self.hp = hp
             return
+        self.bucket_ready(b, compute_stream, **hp)
+
+    def last_ready(self):
+        """For each bucket, the tensor whose gradient the backward pass writes last (the bucket's
+        first tensor: backward runs last layer first) -- callers whose gradients arrive in that
+        order can hook only these and call bucket_ready() (one host call per bucket)."""
+        return [min(m) for m in self.members]
+
+    def bucket_ready(self, b, compute_stream=None, **hp):
+        """Every gradient of bucket b has been written (on compute_stream): launch its collective
+        on the side stream behind an event."""
+        import torch
+        self.hp = hp
+        self.missing[b] = 0
         ev = torch.cuda.Event()
         ev.record(compute_stream or torch.cuda.current_stream())
         self.stream.wait_event(ev)

@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--bucket-mb", type=float, default=25.0)
     ap.add_argument("--ctas", type=int, default=0, help="CTA budget of the bucket launches")
+    ap.add_argument("--split", action="store_true",
+                    help="buckets run the allreduce only; the update runs once at the end")
     a = ap.parse_args()
     import torchvision
 
@@ -70,7 +72,7 @@ def main():
     W, G, D = tc.Group(comm, wv), tc.Group(comm, gv), tc.Group(comm, dv)
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (world * a.batch))
     step = tc.BucketedStep(comm, gv, wv, dv, bucket_bytes=int(a.bucket_mb * (1 << 20)),
-                           ctas=a.ctas)
+                           ctas=a.ctas, split=a.split)
     # one hook per bucket, on the tensor the backward pass writes last in that bucket (autograd
     # visits the layers last to first): one host call per bucket, not per tensor
     last = {id(params[t]): b for b, t in enumerate(step.last_ready())}
@@ -139,7 +141,8 @@ def main():
         print(json.dumps({
             "bench": "resnet50 training step, f1 overlap (PAPER.md:59)", "n_gpus": world,
             "batch_per_gpu": a.batch, "bucket_mb": a.bucket_mb, "buckets": step.nbuckets,
-            "ctas": a.ctas or "auto", "t_compute_us": t_compute, "t_serial_us": t_serial,
+            "ctas": a.ctas or "auto", "mode": "split" if a.split else "fused",
+            "t_compute_us": t_compute, "t_serial_us": t_serial,
             "t_overlap_us": t_overlap, "t_step_alone_us": t_step,
             "hidden_fraction": (t_serial - t_overlap) / max(t_serial - t_compute, 1e-9),
             "speedup_vs_serial": t_serial / t_overlap, "replicas_identical": same,

@@ -10,8 +10,8 @@ init, synthetic 224x224 images and labels; bf16 autocast, fp32 master weights an
 Its 161 parameters are views of one flat weight buffer and its gradients views of one flat
 gradient buffer, so libtc groups wrap the model's own tensors (no copies):
   serial   -- forward + backward, then one tc_sgd_step over the whole group;
-  overlap  -- tc.BucketedStep: a post-accumulate-grad hook on the last-written parameter of
-              every bucket; each bucket's fused allreduce + SGD launches on a side stream as
+  overlap  -- tc.BucketedStep: a post-accumulate-grad hook on every parameter reports its
+              gradient ready; each bucket's fused allreduce + SGD launches on a side stream as
               soon as its last gradient lands (backward order), while the backward continues;
   compute  -- forward + backward alone (no step), the floor.
 Per-iteration device time (CUDA events, max over ranks); hidden fraction = (serial - overlap) /
@@ -73,18 +73,19 @@ def main():
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (world * a.batch))
     step = tc.BucketedStep(comm, gv, wv, dv, bucket_bytes=int(a.bucket_mb * (1 << 20)),
                            ctas=a.ctas, split=a.split)
-    # one hook per bucket, on the tensor the backward pass writes last in that bucket (autograd
-    # visits the layers last to first): one host call per bucket, not per tensor
-    last = {id(params[t]): b for b, t in enumerate(step.last_ready())}
+    # a hook on every parameter: the bucket launches when its last gradient is counted (hooking
+    # only the lowest-index tensor of each bucket is NOT safe -- autograd may accumulate a
+    # layer's weight before its bias, so a bucket could launch before its last gradient lands;
+    # measured: replicas diverged)
+    index = {id(p): t for t, p in enumerate(params)}
     mode = {"hooks": False}
 
     def hook(p):
         if mode["hooks"]:
-            step.bucket_ready(last[id(p)], **hp)
+            step.grad_ready(index[id(p)], **hp)
 
     for p in params:
-        if id(p) in last:
-            p.register_post_accumulate_grad_hook(hook)
+        p.register_post_accumulate_grad_hook(hook)
     x = torch.randn(a.batch, 3, 224, 224, device="cuda")
     y = torch.randint(0, 1000, (a.batch,), device="cuda")
     crit = torch.nn.CrossEntropyLoss()

@@ -498,15 +498,10 @@ class BucketedStep:
             return
         self.bucket_ready(b, compute_stream, **hp)
 
-    def last_ready(self):
-        """For each bucket, the tensor whose gradient the backward pass writes last (the bucket's
-        first tensor: backward runs last layer first) -- callers whose gradients arrive in that
-        order can hook only these and call bucket_ready() (one host call per bucket)."""
-        return [min(m) for m in self.members]
-
     def bucket_ready(self, b, compute_stream=None, **hp):
         """Every gradient of bucket b has been written (on compute_stream): launch its collective
-        on the side stream behind an event."""
+        on the side stream behind an event.  The caller must know that all of them are written
+        (grad_ready counts them); calling it early races the collective with the backward pass."""
         import torch
         self.hp = hp
         self.missing[b] = 0

@@ -1,6 +1,7 @@
 """T2 (real multi-GPU): one process per GPU over CUDA IPC + NVLink, launched with torchrun.
 
-Skipped when fewer than 2 GPUs are visible.  Runs at p = 2 and, when available, at p = 4 and 8.
+Skipped when fewer than 2 GPUs are visible.  Runs at p = 2 and, when available, at p = 3, 4 and 8
+(p = 3: owner chunks of a non-power-of-two split).
 """
 import os
 import socket
@@ -26,7 +27,7 @@ def _free_port():
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
 def test_multiprocess_parity(p):
     if NGPU < p:
         pytest.skip(f"needs {p} GPUs, have {NGPU}")

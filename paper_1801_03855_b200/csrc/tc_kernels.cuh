@@ -794,12 +794,6 @@ __global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
 }
 
 // Low-latency: no barrier; each slot is pushed to every peer and its peers' words awaited.
-#ifndef TC_LL_U
-#define TC_LL_U 0             // 0: one slot per thread; else slots per lane above TC_LL_FLAT_MAX
-#endif
-#ifndef TC_LL_FLAT_MAX
-#define TC_LL_FLAT_MAX 16384  // slots (256 KiB)
-#endif
 template <int OP, int P, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_ll(KParams kp) {
   const int r = kp.rank0 + (int)blockIdx.y;
@@ -807,13 +801,7 @@ __global__ void __launch_bounds__(512, MINB) k_ll(KParams kp) {
   call_begin(kp, r);
   stamp(kp, 0);
   LLBody<OP, P> body{kp, r, (int)(ep() & 1u)};
-#if TC_LL_U > 0
-  // larger groups: every lane pushes TC_LL_U slots before it polls for any (fewer spinning
-  // threads, more stores in flight)
-  if (kp.M > TC_LL_FLAT_MAX) slot_loop<TC_LL_U>(kp, 0, kp.M, body);
-  else
-#endif
-    slot_loop_flat(kp, 0, kp.M, body);
+  slot_loop_flat(kp, 0, kp.M, body);
   call_end(kp, r);
   stamp(kp, 5);
 }

@@ -442,7 +442,9 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     // bytes; the buffers' capacities the padded slot grid.
     const int64_t data_bytes = pl.N * 4;
     const int64_t ll_cap = (int64_t)(kLLBytes / 2 / 8 / p) & ~(size_t)3;
-    const int64_t ll_auto = p == 2 ? kDefaultLLMax : (p <= 4 ? kDefaultLLMax / 2 : kDefaultLLMax / 8);
+    // (p = 2 up to the LL buffer's 2 MiB: at 2 MiB LL 17.4 / 21.2 us for 1 / 161 tensors vs
+    // one-shot 19.9 / 21.2, NCCL 18.7; profiles/r02_latency_probe_ll_p2.jsonl)
+    const int64_t ll_auto = p == 2 ? 2 * kDefaultLLMax : (p <= 4 ? kDefaultLLMax / 2 : kDefaultLLMax / 8);
     const int64_t ll_lim = c.tune_ll < 0 ? ll_auto : c.tune_ll;
     if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
     else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;

@@ -323,3 +323,32 @@ def test_resnet50_easgd_async(p):
     for i in range(p):
         assert_bitwise(got[i][0], wx[i], f"async x p={p} client {i}")
         assert_bitwise(got[i][1], wc, f"async center p={p} replica {i}")
+
+
+# ------------------------------------------------------------------ tensors of >= 2^31 elements
+def test_p1_tensor_over_2g_elements():
+    """A single tensor of 2^31 + 13 fp32 elements (8 GiB) between two small ones on the p = 1
+    TMA stream: tiles past element 2^31 need the 64-bit tile offsets.  With scale 1/2 the result
+    is exactly x / 2 for every finite x (a power-of-two scale rounds nothing) -- a property that
+    holds at any size, checked element by element on the device against a kept copy."""
+    n_big = (1 << 31) + 13
+    free, _ = torch.cuda.mem_get_info()
+    if free < 2.6 * 4 * n_big:
+        pytest.skip("needs ~23 GB of free device memory")
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    xs = [torch.randn(5, device="cuda", generator=gen),
+          torch.randn(n_big, device="cuda", generator=gen),
+          torch.randn(7, device="cuda", generator=gen)]
+    keep = [x.clone() for x in xs]
+    comm = tc.Comm.single(0)
+    g = tc.Group(comm, xs)
+    tc.allreduce(g, 0.5)
+    torch.cuda.synchronize()
+    assert comm.last_launch()[0] == "local"
+    assert comm.async_error() == 0
+    g.destroy()
+    comm.destroy()
+    assert torch.equal(xs[0], keep[0] * 0.5) and torch.equal(xs[2], keep[2] * 0.5)
+    chunk = 1 << 28
+    for lo in range(0, n_big, chunk):
+        assert torch.equal(xs[1][lo:lo + chunk], keep[1][lo:lo + chunk] * 0.5), lo

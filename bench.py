@@ -506,11 +506,18 @@ def main():
                     "peak_source": hbm_src, "algorithmic_bytes_per_launch": hbm_bytes,
                     "kernel": "k_local_tma<OP_SGD>"}
     else:
-        nvl_bytes = 2 * (p - 1) / p * S
-        roofline = {"bound": "nvlink", "achieved": value, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
-                    "frac": value / NVLINK_PEER_GBS, "frac_of_nominal_900": value / NVLINK_NOMINAL_GBS,
-                    "traffic": traffic,
-                    "achieved_is": "algorithmic NVLink bytes per GPU 2(p-1)/p S / CUDA-event time",
+        # the step's own link bytes per GPU per direction: 2(p-1)/p S for the two-shot, (1 + 1/p) S
+        # when the switch reduces (NVLS) -- value stays BASELINE's busbw either way
+        nvls = algo == "nvls"
+        nvl_bytes = (1 + 1 / p) * S if nvls else 2 * (p - 1) / p * S
+        achieved = nvl_bytes / t_s / 1e9
+        roofline = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                    "frac": achieved / NVLINK_PEER_GBS,
+                    "frac_of_nominal_900": achieved / NVLINK_NOMINAL_GBS, "traffic": traffic,
+                    "achieved_is": ("algorithmic NVLink bytes per GPU per direction, (1 + 1/p) S "
+                                    "(switch reduction)" if nvls else
+                                    "algorithmic NVLink bytes per GPU 2(p-1)/p S") +
+                                   " / CUDA-event time",
                     "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
                     "algorithmic_bytes_per_launch": nvl_bytes, "kernel": f"{algo} (OP_SGD)"}
 

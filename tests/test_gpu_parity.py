@@ -646,3 +646,32 @@ def test_easgd_async_single_client_and_errors():
     X.destroy()
     C.destroy()
     comm.destroy()
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_degenerate_groups(p):
+    """Degenerate groups: every tensor empty (the calls are no-ops and succeed), and a single
+    element over p ranks (one owner holds it, the others own nothing)."""
+    comm = tc.Comm.single(0) if p == 1 else tc.Comm.emulated(p, 0)
+    pick = (lambda v: v) if p > 1 else (lambda v: v[0])
+    empty = [[torch.empty(0, device="cuda"), torch.empty(0, device="cuda")] for _ in range(p)]
+    g = tc.Group(comm, pick(empty))
+    tc.allreduce(g, 0.5)
+    tc.sgd_step(g, g, g, lr=0.1)
+    tc.easgd_update(g, g, 0.1)
+    g.destroy()
+    xs = [[np.array([float(k + 1)], np.float32)] for k in range(p)]
+    for algo in ((0, -1, -1), (1, 0, 0), (6, 0, 0), (0, 1 << 20, 0), (0, 0, 1 << 20)):
+        if p > 1:
+            comm.set_algorithm(algo[0])
+            comm.set_tuning(0, 0, algo[1])
+            comm.set_ll_max(algo[2])
+        dev = [to_dev(x) for x in xs]
+        g = tc.Group(comm, pick(dev))
+        tc.allreduce(g, 1.0)
+        want = O.allreduce(xs)
+        for r in range(p):
+            assert_bitwise(to_host(dev[r]), want, f"algo {algo} rank {r}")
+        g.destroy()
+    assert comm.async_error() == 0
+    comm.destroy()

@@ -18,9 +18,16 @@
 //    barrier -> allgather: pull every other owner's staged chunk (rotated start), epilogue.
 //    No exit barrier: peers read only staging, which is rewritten two calls later, after the
 //    next call's first barrier proved every peer finished this one.
+//  * Two-shot, TMA (the default for large groups): the same phases with the data moved by
+//    cp.async.bulk into a shared-memory stage ring (producer warp + consumer warps).
 //  * One-shot (A5, small groups): copy the group into a parity-selected staging buffer, ENTRY
-//    barrier, every rank reduces all slots from all p staging buffers.
-//  * Local (p = 1): the epilogue as a single HBM stream.
+//    barrier, every rank reduces all slots from all p staging buffers.  Low-latency (LL): every
+//    element to every peer as an 8-B {value, epoch} word, no barrier.
+//  * NVLS: the switch reduces and multicasts the owner chunk (tolerance contract), the SGD
+//    epilogue consuming published rounds; the switch broadcast.
+//  * Async-server EASGD: the owner applies the clients' arrivals in order, storing every
+//    client's new chunk into its tensor.
+//  * Local (p = 1): the epilogue as a single HBM stream (TMA).
 //  * Arithmetic: float64 accumulation in canonical rank order (R3/R4) and explicit _rn fp32
 //    ops for the SGD/elastic epilogues (no FMA contraction, R5): GPU == CPU oracle bit for bit.
 #include <cuda_runtime.h>

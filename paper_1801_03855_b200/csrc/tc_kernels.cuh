@@ -785,14 +785,20 @@ __global__ void __launch_bounds__(512, MINB) k_oneshot(KParams kp) {
   call_begin(kp, r);
   const int lo = 0, hi = kp.M;
   stamp(kp, 0);
+  // groups of at most one slot per thread (the runtime sizes the grid for it up to two CTAs per
+  // SM): every thread takes one slot -- its tensor lookup and its p remote loads in parallel
+  // with every other thread's -- instead of a warp walking a 128-slot piece
+  const bool flat = (int64_t)hi <= (int64_t)gridDim.x * blockDim.x;
   {
     CopyOutBody body{kp, r, 0, kp.stage[r] + stage_off()};
-    slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
+    if (flat) slot_loop_flat(kp, lo, hi, body);
+    else slot_loop<unroll_for(1, MINB)>(kp, lo, hi, body);
   }
   if (!barrier_all(kp, r, BAR_ENTRY, true)) return;
   stamp(kp, 1);
   ReduceBody<OP, P, SRC_ONESHOT, false> body{kp, r, 0, nullptr};
-  slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
+  if (flat) slot_loop_flat(kp, lo, hi, body);
+  else slot_loop<unroll_for(P, MINB)>(kp, lo, hi, body);
   stamp(kp, 2);
   stamp(kp, 3);
   stamp(kp, 4);

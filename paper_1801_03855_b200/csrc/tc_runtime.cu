@@ -444,7 +444,9 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     const int64_t ll_cap = (int64_t)(kLLBytes / 2 / 8 / p) & ~(size_t)3;
     // (p = 2 up to the LL buffer's 2 MiB: at 2 MiB LL 17.4 / 21.2 us for 1 / 161 tensors vs
     // one-shot 19.9 / 21.2, NCCL 18.7; profiles/r02_latency_probe_ll_p2.jsonl)
-    const int64_t ll_auto = p == 2 ? 2 * kDefaultLLMax : (p <= 4 ? kDefaultLLMax / 2 : kDefaultLLMax / 8);
+    // (p = 3, 4 only up to 256 KiB: from 512 KiB the flat one-shot wins, p = 4 512 KiB 14.4 /
+    // 16.0 us vs LL 17.1 / 18.1 for 1 / 161 tensors, profiles/r02_latency_probe_os_p4.jsonl)
+    const int64_t ll_auto = p == 2 ? 2 * kDefaultLLMax : (p <= 4 ? kDefaultLLMax / 4 : kDefaultLLMax / 8);
     const int64_t ll_lim = c.tune_ll < 0 ? ll_auto : c.tune_ll;
     if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
     else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;
@@ -485,6 +487,10 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     kp.ntiles = ga->ntiles;
   } else if (twoshot && tune_ctas > 0) {
     ctas = tune_ctas;
+  } else if (algo == ALGO_ONESHOT && want <= (int64_t)c.num_sms * occ / nlocal) {
+    // one slot per thread (the kernel's flat path): every slot's p remote loads in flight at
+    // once -- p = 4, 1 MiB: 16.9-18.6 us against 21.3-23.8 for pieces walked by warps
+    ctas = (int)want;
   } else {
     ctas = (int)std::min<int64_t>(
         want, (int64_t)c.num_sms * ((algo == ALGO_ONESHOT || algo == ALGO_LL) ? 1 : occ));

@@ -136,8 +136,8 @@ TC_API tc_status tc_comm_create_emulated(int nranks, int cuda_device, tc_comm** 
  * calls.  Errors: TC_ERR_INVALID_ARG. */
 TC_API tc_status tc_comm_set_tuning(tc_comm* comm, int num_ctas, int threads, int64_t oneshot_max_bytes);
 
-/* Groups of at most `bytes` of data (-1 = automatic: 2 MiB at p = 2, 256 KiB at p <= 4,
- * 128 KiB beyond; 0 = never) use the low-latency algorithm:
+/* Groups of at most `bytes` of data (-1 = automatic: 1 MiB at p = 2, 512 KiB at p = 3,
+ * 256 KiB at p = 4, 128 KiB beyond; 0 = never) use the low-latency algorithm:
  * every rank stores each element to every peer as one 8-byte {value, call epoch} word and waits
  * for its peers' words in local memory, so a call costs one NVLink crossing and no barrier.
  * Same arithmetic (float64, rank order) as the other P2P algorithms.  Capped by the LL buffer

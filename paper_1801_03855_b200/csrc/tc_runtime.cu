@@ -442,11 +442,12 @@ tc_status run_hot(int op, Group* ga, Group* gb, Group* gc, float scale, float lr
     // bytes; the buffers' capacities the padded slot grid.
     const int64_t data_bytes = pl.N * 4;
     const int64_t ll_cap = (int64_t)(kLLBytes / 2 / 8 / p) & ~(size_t)3;
-    // (p = 2 up to the LL buffer's 2 MiB: at 2 MiB LL 17.4 / 21.2 us for 1 / 161 tensors vs
-    // one-shot 19.9 / 21.2, NCCL 18.7; profiles/r02_latency_probe_ll_p2.jsonl)
-    // (p = 3, 4 only up to 256 KiB: from 512 KiB the flat one-shot wins, p = 4 512 KiB 14.4 /
-    // 16.0 us vs LL 17.1 / 18.1 for 1 / 161 tensors, profiles/r02_latency_probe_os_p4.jsonl)
-    const int64_t ll_auto = p == 2 ? 2 * kDefaultLLMax : (p <= 4 ? kDefaultLLMax / 4 : kDefaultLLMax / 8);
+    // Against the flat one-shot (one slot per thread, profiles/r02_latency_probe_flat.jsonl,
+    // 1 / 161 tensors): p = 2 LL up to 1 MiB (1 MiB 12.6 / 12.2 us vs 13.7 / 15.4; 2 MiB 17.3 /
+    // 21.4 vs 14.6 / 21.3); p = 3 up to 512 KiB (13.9 / 13.8 vs 13.8 / 15.8; 1 MiB 22.1 vs
+    // 15.1); p = 4 up to 256 KiB (512 KiB 17.2 / 18.3 vs 14.5 / 16.4).
+    const int64_t ll_auto = p == 2 ? kDefaultLLMax : p == 3 ? kDefaultLLMax / 2
+                          : p == 4 ? kDefaultLLMax / 4 : kDefaultLLMax / 8;
     const int64_t ll_lim = c.tune_ll < 0 ? ll_auto : c.tune_ll;
     if (data_bytes <= ll_lim && 4 * Mdev <= ll_cap) algo = ALGO_LL;
     else if (data_bytes <= lim && bytes <= (int64_t)kStageCapacity) algo = ALGO_ONESHOT;

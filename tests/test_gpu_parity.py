@@ -94,6 +94,35 @@ def test_random_groups_grad_values(p, name, oneshot):
         assert (np.abs(out[0][t] - ref[t]) <= bound).all()
 
 
+@pytest.mark.parametrize("extra", [-1, 0, 1, 515])
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_oneshot_flat_boundary(p, extra):
+    """The one-shot deals one slot per thread when the group's M slots fit a grid of up to
+    2 CTAs/SM per local rank (512 threads), else 128-slot pieces over that grid: groups of
+    limit-1, limit, limit+1 and limit+515 slots (ragged tensors, 2 tails) stay bit-exact."""
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    limit = (2 * sms // p) * 512
+    m = limit + extra
+    numels = [4 * (m // 3) - 1, 4 * (m // 3) - 2]
+    numels.append(4 * (m - 2 * (m // 3)))
+    assert tc.Plan(numels).num_slots == m
+    xs = [W.group(numels, "int", 900 + extra, 0, k, W.GRAD) for k in range(p)]
+    comm = _comm(p, 8 << 20)
+    dev = [to_dev(x) for x in xs]
+    grp = tc.Group(comm, dev)
+    tc.allreduce(grp, 0.5)
+    algo, ctas, _ = comm.last_launch()
+    assert algo == "one-shot"
+    assert ctas == (-(-m // 512) if extra <= 0 else 2 * sms // p), ctas
+    want = O.allreduce(xs, 0.5)
+    for r in range(p):
+        assert_bitwise(to_host(dev[r]), want, f"rank {r}")
+    assert comm.async_error() == 0
+    grp.destroy()
+    comm.destroy()
+
+
 @pytest.mark.parametrize("offset", [1, 2, 3, "per-rank"])
 @pytest.mark.parametrize("p", [1, 2, 4])
 def test_unaligned_tensors(p, offset):

@@ -123,6 +123,9 @@ def main():
     ap.add_argument("--green", type=int, default=0,
                     help="run the backward pass in a CUDA green context of (SMs - GREEN) SMs, so "
                          "GREEN SMs stay free for the collective (budget GREEN CTAs)")
+    ap.add_argument("--sym", action="store_true",
+                    help="gradients in symmetric (multicast) memory, so --algo 4 (NVLS: the "
+                         "switch reduces; link-bound on ~32 SMs) can run the buckets")
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -143,6 +146,10 @@ def main():
     w_flat, w = flat("param", W.PARAM)
     d_flat, dw = flat("dw", W.DW)
     comm = tc.Comm.single(local) if world == 1 else tc.Comm.from_process_group(device=local)
+    if a.sym and world > 1:
+        g_flat = comm.alloc_symmetric(N)
+        g_flat.copy_(gp_flat)
+        g = list(torch.split(g_flat, numels))
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (world * 128))
     G, Wg, D = tc.Group(comm, g), tc.Group(comm, w), tc.Group(comm, dw)
 
@@ -273,7 +280,7 @@ def main():
                      "buckets": step.nbuckets, "bucket_mb": a.bucket_mb,
                      "ratio": a.ratio, "compute": a.compute, "compute_units": units,
                      "sm_carveout": carve, "green_context_sms_reserved": a.green or None,
-                     "side_stream_priority": bool(a.priority),
+                     "side_stream_priority": bool(a.priority), "grad_memory_symmetric": a.sym,
                      "t_step_us": t_step, "t_compute_us": t_compute,
                      "t_compute_carveout_us": t_comp_c, "t_serial_us": t_serial,
                      "t_overlap_us": t_over,

@@ -50,6 +50,9 @@ def main():
     ap.add_argument("--rounds", type=int, default=5, help="interleaved timing rounds per mode")
     ap.add_argument("--priority", action="store_true",
                     help="bucket launches on a highest-priority side stream")
+    ap.add_argument("--switch", action="store_true",
+                    help="gradients in symmetric memory and the bucket allreduces on the switch "
+                         "(NVLS, algorithm 4: link-bound on ~32 SMs; tolerance contract)")
     ap.add_argument("--channels-last", action="store_true",
                     help="NHWC activations and conv weights (the fast cuDNN layout)")
     a = ap.parse_args()
@@ -69,8 +72,14 @@ def main():
     numels = [p.numel() for p in params]
     N = sum(numels)
     # the weights and gradients as views of flat buffers (the layout libtc and DDP buckets use)
+    comm = tc.Comm.single(local) if world == 1 else tc.Comm.from_process_group(device=local)
     w_flat = torch.empty(N, device="cuda")
-    g_flat = torch.zeros(N, device="cuda")
+    if a.switch and world > 1:
+        g_flat = comm.alloc_symmetric(N)
+        g_flat.zero_()
+        comm.set_algorithm(4)
+    else:
+        g_flat = torch.zeros(N, device="cuda")
     d_flat = torch.zeros(N, device="cuda")
     def as_param(flat, p):
         # a view of the flat slice with p's shape (NHWC strides for conv weights if --channels-last)
@@ -89,7 +98,6 @@ def main():
     wv = list(torch.split(w_flat, numels))
     gv = list(torch.split(g_flat, numels))
     dv = list(torch.split(d_flat, numels))
-    comm = tc.Comm.single(local) if world == 1 else tc.Comm.from_process_group(device=local)
     W, G, D = tc.Group(comm, wv), tc.Group(comm, gv), tc.Group(comm, dv)
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (world * a.batch))
     step = tc.BucketedStep(comm, gv, wv, dv, bucket_bytes=int(a.bucket_mb * (1 << 20)),
@@ -194,7 +202,8 @@ def main():
             "bench": "resnet50 training step, f1 overlap (PAPER.md:59)", "n_gpus": world,
             "batch_per_gpu": a.batch, "bucket_mb": a.bucket_mb, "buckets": step.nbuckets,
             "ctas": a.ctas or "auto", "mode": "split" if a.split else "fused",
-            "graph": a.graph, "channels_last": cl,
+            "graph": a.graph, "channels_last": cl, "switch": a.switch,
+            "algo": comm.last_launch()[0],
             "t_compute_us": t_compute, "t_serial_us": t_serial,
             "t_overlap_us": t_overlap, "t_step_alone_us": t_step,
             "hidden_fraction": (t_serial - t_overlap) / max(t_serial - t_compute, 1e-9),

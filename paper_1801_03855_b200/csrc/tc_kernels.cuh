@@ -1440,6 +1440,9 @@ constexpr int kNvlsWarps = kNvlsThreads / 32;
 #ifndef TC_NV_RED_U_SGD
 #define TC_NV_RED_U_SGD 4  // fused SGD: switch reductions in flight per lane
 #endif
+#ifndef TC_NV_RED_U_AR
+#define TC_NV_RED_U_AR 4   // allreduce: switch reductions in flight per lane
+#endif
 #ifndef TC_NV_EPI_U
 #define TC_NV_EPI_U 4   // fused SGD epilogue: 16-B slots per thread in flight
 #endif
@@ -1496,7 +1499,7 @@ __device__ __forceinline__ void nv_reduce_tile(const KParams& kp, const NvTile& 
     return OP == OP_ALLREDUCE ? __double2float_rn(__dmul_rn((double)v, (double)kp.scale)) : v;
   };
   if (vec) {
-    constexpr int U = OP == OP_SGD ? TC_NV_RED_U_SGD : 4;  // switch reductions in flight per lane
+    constexpr int U = OP == OP_SGD ? TC_NV_RED_U_SGD : TC_NV_RED_U_AR;  // in flight per lane
     for (int s0 = lane_id; s0 < d.n; s0 += 32 * U) {
       float4 v[U];
 #pragma unroll

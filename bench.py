@@ -382,6 +382,48 @@ def claim_stdout():
     return out
 
 
+def p2p_pull_peak(S, p, rank, local, stream, timed_us):
+    """The roofline against a P2P peak measured in the same run: every GPU
+    pulls S/p from every peer at once with TMA bulk copies (tools/nvl_probe.cu, our kernel, no
+    arithmetic) -- GB/s per GPU per direction, best of two launch shapes from the probe sweep
+    (profiles/r02_nvl_probe_p*.jsonl)."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    so = os.path.join(ROOT, "tools", "bin", "libnvl_probe.so")
+    if not os.path.exists(so):
+        return {"unavailable": "tools/bin/libnvl_probe.so not built (__graft_entry__.build)"}
+    try:
+        import torch.distributed._symmetric_memory as symm
+        lib = ctypes.CDLL(so)
+        try:
+            symm.enable_symm_mem_for_group(dist.group.WORLD.group_name)
+        except Exception:  # noqa: BLE001 -- not needed on newer torch
+            pass
+        buf = symm.empty(S // 4, dtype=torch.float32, device=f"cuda:{local}")
+        hdl = symm.rendezvous(buf, dist.group.WORLD.group_name)
+        arr = (ctypes.c_void_p * 8)(*[hdl.buffer_ptrs[q] for q in range(p) if q != rank])
+        part = (S // p) - (S // p) % (1 << 16)
+        rows = []
+        for ctas, tile, depth in ((148, 16384, 12), (32, 32768, 6)):
+            c = max(1, ctas // (p - 1)) * (p - 1)
+            st = ctypes.c_void_p(stream.cuda_stream)
+
+            def f(c=c, tile=tile, depth=depth, st=st):
+                if lib.probe_tma(0, arr, p - 1, ctypes.c_long(part), tile, depth, c, rank, st):
+                    raise RuntimeError("probe_tma launch failed")
+            t = timed_us(f)
+            rows.append({"gbs_per_dir": (p - 1) * part / t / 1e3, "t_us": t, "ctas": c,
+                         "tile_bytes": tile, "stages": depth})
+        torch.cuda.synchronize()
+        del hdl, buf
+        best = max(rows, key=lambda r: r["gbs_per_dir"])
+        return dict(best, kernel="tma_pull_kernel (tools/nvl_probe.cu): all peers at once, "
+                    f"(p-1) x {part} B ingress per GPU", shapes=rows)
+    except Exception as e:  # noqa: BLE001 -- a diagnostic field, never the bench's value
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+
+
 def main():
     jsonout = claim_stdout()
     ap = argparse.ArgumentParser()
@@ -536,6 +578,11 @@ def main():
                 stream.synchronize()
             return max_over_ranks(e0.elapsed_time(e1) / K, world) * 1e3
 
+        # the same-run P2P ceiling: an all-peer TMA pull copy, no arithmetic
+        roofline["p2p_pull_peak"] = p2p_pull_peak(S, p, rank, local, stream, timed_us)
+        pk = roofline["p2p_pull_peak"].get("gbs_per_dir")
+        if pk:
+            roofline["frac_of_p2p_pull_peak"] = achieved / pk
         # allreduce alone (scale 1/p keeps the values fixed from call to call)
         ta = timed_us(lambda: tc.allreduce(G, 1.0 / p, stream=stream))
         extra["allreduce_only"] = {"t_us": ta, "busbw_gbs": 2 * (p - 1) / p * S / ta / 1e3,

@@ -83,6 +83,22 @@ def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False,
     return out
 
 
+PROBE_SRC = os.path.join(ROOT, "tools", "nvl_probe.cu")
+PROBE_LIB = os.path.join(ROOT, "tools", "bin", "libnvl_probe.so")
+
+
+def build_probe(force: bool = False) -> str:
+    """tools/nvl_probe.cu -> tools/bin/libnvl_probe.so: the all-peer copy kernels bench.py runs
+    beside the step as the same-run P2P ceiling; not part of libtc."""
+    if not force and os.path.exists(PROBE_LIB) and \
+            os.path.getmtime(PROBE_LIB) >= os.path.getmtime(PROBE_SRC):
+        return PROBE_LIB
+    os.makedirs(os.path.dirname(PROBE_LIB), exist_ok=True)
+    subprocess.check_call([NVCC, "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
+                           "-shared", "-Xcompiler", "-fPIC", "-o", PROBE_LIB, PROBE_SRC])
+    return PROBE_LIB
+
+
 if __name__ == "__main__":
     import argparse
     ap = argparse.ArgumentParser()

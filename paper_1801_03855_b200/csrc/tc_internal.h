@@ -56,6 +56,14 @@ constexpr int kT2Slots = TC_T2_SLOTS;
 // measured faster there (allreduce 172 vs 175 us, fused step 173 vs 185 us); 512 elsewhere
 constexpr int t2_slots(int p) { return p == 2 ? 2 * kT2Slots : kT2Slots; }
 constexpr int kT2SmemCap = TC_T2_SMEM;
+// The fused SGD step runs faster with fewer bytes in flight per SM (tools/algo_bench.py, ring
+// caps 128 / 160 / 192 KiB: p = 4 step 268.5-269.3 / 268.4-269.4 / 274.5-276.4 us, p = 2
+// 188.3-188.4 / 188.3-188.4 / 191.4-192.5; allreduce and EASGD flat within 1 us;
+// profiles/r02_ring_p24.txt): 160 KiB keeps two stages at p = 8
+#ifndef TC_T2_SMEM_SGD
+#define TC_T2_SMEM_SGD (160 * 1024)
+#endif
+constexpr int t2_cap(int op) { return op == 1 ? TC_T2_SMEM_SGD : kT2SmemCap; }
 constexpr int kT2MaxStages = 16;
 #ifndef TC_T2_CW
 #define TC_T2_CW 8
@@ -77,7 +85,7 @@ constexpr int t2_ops(int op, int p) {
   return rs > ag ? rs : ag;
 }
 constexpr int t2_stages(int op, int p) {
-  const int n = kT2SmemCap / (t2_ops(op, p) * t2_slots(p) * 16);
+  const int n = t2_cap(op) / (t2_ops(op, p) * t2_slots(p) * 16);
   return n > kT2MaxStages ? kT2MaxStages : n;
 }
 constexpr int t2_smem(int op, int p) {

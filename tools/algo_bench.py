@@ -1,6 +1,6 @@
 """Quick per-algorithm timing on the ResNet-50 group (diagnostics, not the bench contract).
 
-    torchrun --nproc-per-node N tools/algo_bench.py [--algos 6,4] [--steps 50] [--ops ar,sgd]
+    torchrun --nproc-per-node N tools/algo_bench.py [--algos 6,4] [--steps 50] [--ops ar,sgd,bc,ea]
 
 Gradients in tc_mem_alloc memory (NVLS-eligible), refreshed before every fused step; CUDA events
 around each kernel, max over ranks.  One JSON line per (op, algo) on rank 0.
@@ -43,6 +43,8 @@ def main():
     dw = torch.from_numpy(np.concatenate(W.group(numels, "dw", 2, 0, 0, W.DW))).cuda()
     split = lambda f: list(torch.split(f, numels))  # noqa: E731
     G, Wg, D = tc.Group(comm, split(g_flat)), tc.Group(comm, split(w)), tc.Group(comm, split(dw))
+    center = torch.from_numpy(np.concatenate(W.group(numels, "param", 3, 0, 0, W.PARAM))).cuda()
+    C = tc.Group(comm, split(center))
     s = torch.cuda.Stream()
     for op in a.ops.split(","):
         for algo in [int(x) for x in a.algos.split(",")]:
@@ -58,6 +60,8 @@ def main():
                         tc.allreduce(G, 1.0 / p, stream=s)
                     elif op == "bc":
                         tc.broadcast(G, 0, stream=s)
+                    elif op == "ea":  # elastic averaging, one client per rank (c = p)
+                        tc.easgd_update(Wg, C, 0.1, stream=s)
                     else:
                         tc.sgd_step(Wg, G, D, lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (128 * p),
                                     stream=s)
@@ -72,7 +76,7 @@ def main():
                 print(json.dumps({"p": p, "op": op, "algo": name, "ctas": ctas, "median_us": t[0].item(),
                                   "mean_us": t[1].item(),
                                   "busbw_gbs": 2 * (p - 1) / p * S / t[1].item() / 1e3}), flush=True)
-    for grp in (G, Wg, D):
+    for grp in (G, Wg, D, C):
         grp.destroy()
     comm.free_symmetric(g_flat)
     comm.destroy()

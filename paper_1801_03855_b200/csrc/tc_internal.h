@@ -27,7 +27,8 @@ constexpr int64_t kDefaultOneshotMax = 256 << 10;
 constexpr int kPieceShift = 7;                 // work piece = 128 slots = 2 KiB per operand
 constexpr int kPiece = 1 << kPieceShift;
 // p = 1 TMA stream (k_local_tma): tiles of up to kTileE elements inside one tensor, kTmaStages
-// shared-memory stages of (up to) three operands, one producer warp + kTmaConsumerWarps.
+// x 3 tiles of shared-memory stages (tc_kernels.cuh local_stages), one producer warp +
+// kTmaConsumerWarps.
 #ifndef TC_TILE_E
 #define TC_TILE_E 2048
 #endif
@@ -41,8 +42,6 @@ constexpr int kTileE = TC_TILE_E;
 constexpr int kTmaStages = TC_TMA_STAGES;
 constexpr int kTmaConsumerWarps = TC_TMA_CW;
 constexpr int kTmaThreads = 32 * (1 + kTmaConsumerWarps);
-constexpr int kTmaSmem = kTmaStages * 3 * kTileE * 4;      // three operands (SGD: g, w, dw)
-constexpr int kTmaSmem4 = kTmaStages * 4 * kTileE * 4;     // four (ESGD: x, center, dw, g)
 // Two-shot, TMA-staged (k_twoshot_tma): owner-chunk tiles of <= kT2Slots slots inside one
 // tensor; each stage holds every operand of one tile; as many stages as fit kT2SmemCap.
 #ifndef TC_T2_SLOTS
@@ -99,6 +98,19 @@ constexpr int kNvlsThreads = 512;              // NVLS: 16 warps (reduction / si
 constexpr int kNvSlots = TC_NV_SLOTS;           // NVLS tile: <= 512 slots = 8 KiB per operand
 enum Barrier { BAR_ENTRY = 0, BAR_MID = 1, BAR_PROG = 2 };  // PROG: NVLS round progress
 enum Op { OP_ALLREDUCE = 0, OP_SGD = 1, OP_EASGD = 2, OP_ESGD = 3, OP_BCAST = 4, OP_EASYNC = 5 };
+// p = 1 TMA stream: operands per stage -- g (SGD: + w, dw), x + center (EASGD, async EASGD),
+// x, center, dw, g (fused elastic + SGD) -- and stages: the ring holds kTmaStages x 3 tiles
+// (96 KiB, two CTAs per SM) whatever the count, so every op keeps the SGD step's bytes in flight
+// (allreduce 12 stages, EASGD 6, SGD 4, fused elastic + SGD 3).  tc_kernels.cuh checks the
+// counts against the kernels' operand needs.
+constexpr int local_ops(int op) {
+  return op == OP_SGD ? 3 : (op == OP_EASGD || op == OP_EASYNC) ? 2 : op == OP_ESGD ? 4 : 1;
+}
+constexpr int kTmaMaxStages = 12;
+constexpr int local_stages(int na) {
+  return kTmaStages * 3 / na < kTmaMaxStages ? kTmaStages * 3 / na : kTmaMaxStages;
+}
+constexpr int local_smem(int op) { return local_stages(local_ops(op)) * local_ops(op) * kTileE * 4; }
 enum Algo {
   ALGO_LOCAL = 0,
   ALGO_TWOSHOT = 1,

@@ -30,8 +30,7 @@ struct Shape {
   int smem;
 };
 Shape shape_of(int op, int algo, int p, int threads) {
-  if (algo == ALGO_LOCAL)
-    return {kTmaThreads, op == OP_ESGD ? kTmaSmem4 : kTmaSmem};
+  if (algo == ALGO_LOCAL) return {kTmaThreads, local_smem(op)};
   if (algo == ALGO_TWOSHOT_TMA) return {kT2Threads, t2_smem(op, p)};
   if (algo == ALGO_NVLS) return {kNvlsThreads, 0};
   return {threads, 0};

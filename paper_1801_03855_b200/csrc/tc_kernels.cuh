@@ -185,6 +185,13 @@ template <int OP, int PH, int P> struct Needs {
   static constexpr bool storeC = (OP == OP_SGD) || (OP == OP_ESGD);
 };
 
+// p = 1 TMA stream: operands per stage from the kernels' needs (must match local_ops()).
+template <int OP>
+__host__ __device__ constexpr int local_na() {
+  using N = Needs<OP, PH_RS, 1>;
+  return 1 + (N::loadB ? 1 : 0) + (N::loadC ? 1 : 0) + (N::loadD ? 1 : 0);
+}
+
 // SGD epilogue (A6), fp32 mirror of the oracle: t = R(R(rs*G)+R(wd*w)); dw' = R(R(mu*dw)-R(lr*t));
 // w' = R(w+dw').
 __device__ __forceinline__ void sgd1(const KParams& kp, float G, float& w, float& dw) {
@@ -840,7 +847,7 @@ __device__ __forceinline__ int64_t tile_elem(const int4& tl) {
 // p = 1 (no communication): the epilogue as one HBM stream, moved by the copy engine of each
 // SM.  Tiles (<= kTileE elements inside one tensor, group-creation table) are dealt round-robin
 // over the grid (DRAM locality, as the pieces of the other kernels); lane 0 of warp 0 issues
-// cp.async.bulk loads of the tile's operands into kTmaStages shared-memory stages (mbarrier
+// cp.async.bulk loads of the tile's operands into local_stages() shared-memory stages (mbarrier
 // complete_tx), the consumer warps apply elem<> from shared memory and store 16-B vectors.
 // Tiles that are not 16-B aligned in every operand (or a tensor's last numel % 4 elements) are
 // processed element by element straight from global memory, with the same arithmetic.
@@ -849,14 +856,16 @@ __device__ __forceinline__ int64_t tile_elem(const int4& tl) {
 template <int OP>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
   using N = Needs<OP, PH_RS, 1>;
-  constexpr int NA = 1 + (N::loadB ? 1 : 0) + (N::loadC ? 1 : 0) + (N::loadD ? 1 : 0);
-  constexpr int NSLOT = N::loadD ? 4 : 3;  // operand slots per stage (kTmaSmem / kTmaSmem4)
-  extern __shared__ __align__(128) float4 sm4[];  // [kTmaStages][NSLOT][kTileE / 4]
-  __shared__ __align__(8) uint64_t full[kTmaStages], empty[kTmaStages];
+  constexpr int NA = local_na<OP>();            // operands per stage, packed: a, [b], [c], [d]
+  static_assert(NA == local_ops(OP), "local_ops() disagrees with the operand needs");
+  constexpr int NST = local_stages(NA);
+  constexpr int IB = 1, IC = IB + (N::loadB ? 1 : 0), ID = IC + (N::loadC ? 1 : 0);
+  extern __shared__ __align__(128) float4 sm4[];  // [NST][NA][kTileE / 4]
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
   const int r = kp.rank0 + (int)blockIdx.y;
   const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < NST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[s])),
                    "r"(kTmaConsumerWarps));
@@ -876,8 +885,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
     if (lane_id != 0) return;
     int k = 0;
     for (int i = blockIdx.x; i < kp.ntiles; i += gridDim.x, ++k) {
-      const int s = k % kTmaStages;
-      if (k >= kTmaStages) mbar_wait(&empty[s], (uint32_t)((k / kTmaStages - 1) & 1));
+      const int s = k % NST;
+      if (k >= NST) mbar_wait(&empty[s], (uint32_t)((k / NST - 1) & 1));
       const int4 tl = kp.tiles[i];
       const int64_t e0 = tile_elem(tl);
       if (!aligned(tl.x, e0, tl.z)) {  // consumers read global memory directly
@@ -894,14 +903,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
                              N::loadB ? kp.b[row + tl.x] + e0 : nullptr,
                              N::loadC ? kp.c[row + tl.x] + e0 : nullptr,
                              N::loadD ? kp.d[row + tl.x] + e0 : nullptr};
+      int slot = 0;
 #pragma unroll
-      for (int o = 0; o < NSLOT; ++o) {
+      for (int o = 0; o < 4; ++o) {
         if (src[o] == nullptr) continue;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-            "[%3];" ::"r"(smem_u32(sm4 + ((size_t)s * NSLOT + o) * (kTileE / 4))),
+            "[%3];" ::"r"(smem_u32(sm4 + ((size_t)s * NA + slot) * (kTileE / 4))),
             "l"(src[o]), "r"(bytes), "r"(smem_u32(&full[s]))
             : "memory");
+        ++slot;
       }
     }
     return;
@@ -909,19 +920,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
   const int ct = threadIdx.x - 32, nct = kTmaThreads - 32;
   int k = 0;
   for (int i = blockIdx.x; i < kp.ntiles; i += gridDim.x, ++k) {
-    const int s = k % kTmaStages;
+    const int s = k % NST;
     const int4 tl = kp.tiles[i];
     const int64_t e0 = tile_elem(tl);
     float* pa = kp.a[row + tl.x] + e0;
     float* pb = (N::loadB || N::storeB) ? kp.b[row + tl.x] + e0 : nullptr;
     float* pc = (N::loadC || N::storeC) ? kp.c[row + tl.x] + e0 : nullptr;
     const float* pd = N::loadD ? kp.d[row + tl.x] + e0 : nullptr;
-    mbar_wait(&full[s], (uint32_t)((k / kTmaStages) & 1));
+    mbar_wait(&full[s], (uint32_t)((k / NST) & 1));
     if (aligned(tl.x, e0, tl.z)) {
-      const float4* sa = sm4 + ((size_t)s * NSLOT + 0) * (kTileE / 4);
-      const float4* sb = sm4 + ((size_t)s * NSLOT + 1) * (kTileE / 4);
-      const float4* sc = sm4 + ((size_t)s * NSLOT + 2) * (kTileE / 4);
-      const float4* sd = sm4 + ((size_t)s * NSLOT + 3) * (kTileE / 4);
+      const float4* sa = sm4 + ((size_t)s * NA + 0) * (kTileE / 4);
+      const float4* sb = sm4 + ((size_t)s * NA + IB) * (kTileE / 4);
+      const float4* sc = sm4 + ((size_t)s * NA + IC) * (kTileE / 4);
+      const float4* sd = sm4 + ((size_t)s * NA + ID) * (kTileE / 4);
       for (int v = ct; v < tl.z / 4; v += nct) {
         const float4 va = sa[v];
         float4 vb = N::loadB ? sb[v] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -965,7 +976,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_local_tma(KParams kp) {
 // reduce-scatter, the owner's staged chunk in the allgather, plus the local epilogue operands --
 // into a ring of shared-memory stages, a stage holding G tiles when a phase has fewer operands
 // than the stage has room for.  8 consumer warps reduce (float64, rank order), apply the
-// epilogue and store.  Bytes in flight per CTA = the ring (up to 160 KiB), not one register
+// epilogue and store.  Bytes in flight per CTA = the ring (up to 192 KiB), not one register
 // load per thread, so a few CTAs drive the links and the other SMs stay free for computation
 // running beside the collective (NEXT row f1).  Same tiles-to-CTA pairing (tile i of a chunk ->
 // CTA i mod grid on every rank), staging, barriers and arithmetic as k_twoshot_pull.

@@ -48,6 +48,9 @@ def main():
                     help="capture each mode's whole iteration in one CUDA graph and time replays "
                          "(no host launch cost; the bucket kernels hang off the graph's edges)")
     ap.add_argument("--rounds", type=int, default=5, help="interleaved timing rounds per mode")
+    ap.add_argument("--threads", type=int, default=0,
+                    help="threads per CTA of the NVLS allreduce (with --switch --split: small CTAs "
+                         "that can sit beside the backward pass's CTAs)")
     ap.add_argument("--priority", action="store_true",
                     help="bucket launches on a highest-priority side stream")
     ap.add_argument("--switch", action="store_true",
@@ -78,6 +81,7 @@ def main():
         g_flat = comm.alloc_symmetric(N)
         g_flat.zero_()
         comm.set_algorithm(4)
+        comm.set_tuning(0, a.threads, -1)
     else:
         g_flat = torch.zeros(N, device="cuda")
     d_flat = torch.zeros(N, device="cuda")
@@ -202,7 +206,7 @@ def main():
             "bench": "resnet50 training step, f1 overlap (PAPER.md:59)", "n_gpus": world,
             "batch_per_gpu": a.batch, "bucket_mb": a.bucket_mb, "buckets": step.nbuckets,
             "ctas": a.ctas or "auto", "mode": "split" if a.split else "fused",
-            "graph": a.graph, "channels_last": cl, "switch": a.switch,
+            "graph": a.graph, "channels_last": cl, "switch": a.switch, "threads": a.threads or 512,
             "algo": comm.last_launch()[0],
             "t_compute_us": t_compute, "t_serial_us": t_serial,
             "t_overlap_us": t_overlap, "t_step_alone_us": t_step,

@@ -128,9 +128,10 @@ TC_API tc_status tc_comm_create(int rank, int nranks, int cuda_device, tc_allgat
  * local pointers).  Not collective. */
 TC_API tc_status tc_comm_create_emulated(int nranks, int cuda_device, tc_comm** out);
 
-/* Launch tuning, must be identical on all ranks.  num_ctas: CTAs per rank for two-shot calls
- * (0 = automatic: a full wave of the GPU); threads: threads per CTA (0 = 512; a multiple of 32
- * in [64, 1024]); oneshot_max_bytes: groups of at most this many bytes use the one-shot
+/* Launch tuning, must be identical on all ranks.  num_ctas: CTAs per rank for two-shot and NVLS
+ * calls (0 = automatic: a full wave of the GPU); threads: threads per CTA of the register kernels
+ * and of the NVLS allreduce (0 = 512; a multiple of 32 in [64, 512]; the TMA kernels and the
+ * NVLS fused step keep their fixed block sizes); oneshot_max_bytes: groups of at most this many bytes use the one-shot
  * algorithm (-1 = automatic: 8 MiB at p = 2, 4 MiB at p = 3, 2 MiB at p = 4, 256 KiB beyond;
  * 0 = never; capped by the staging capacity).  Applies to later
  * calls.  Errors: TC_ERR_INVALID_ARG. */

@@ -32,7 +32,8 @@ struct Shape {
 Shape shape_of(int op, int algo, int p, int threads) {
   if (algo == ALGO_LOCAL) return {kTmaThreads, local_smem(op)};
   if (algo == ALGO_TWOSHOT_TMA) return {kT2Threads, t2_smem(op, p)};
-  if (algo == ALGO_NVLS) return {kNvlsThreads, 0};
+  // NVLS: the allreduce takes the comm's thread count (>= 2 warps), the other ops 512
+  if (algo == ALGO_NVLS) return {op == OP_ALLREDUCE ? threads : kNvlsThreads, 0};
   return {threads, 0};
 }
 

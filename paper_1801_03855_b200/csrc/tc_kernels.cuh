@@ -1597,8 +1597,12 @@ __device__ __forceinline__ bool nv_wait(const KParams& kp, int r, int q, int rou
 
 template <int OP, int P>
 __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
-  constexpr int NW = nvls_reduce_warps(OP);  // switch-reduction warps; warp NW signals
-  constexpr int NE = kNvlsWarps - NW - 1;    // SGD epilogue warps
+  // switch-reduction warps; warp NW signals.  The allreduce runs any block size of >= 2 warps
+  // (up to 12 reduction warps; a 4-warp CTA can fit beside a compute kernel's CTA -- NEXT row
+  // f1); the fused step has the fixed 16-warp split.
+  const int NW = OP == OP_ALLREDUCE ? min(nvls_reduce_warps(OP), (int)(blockDim.x >> 5) - 1)
+                                    : nvls_reduce_warps(OP);
+  constexpr int NE = kNvlsWarps - nvls_reduce_warps(OP) - 1;  // SGD epilogue warps
   const int r = kp.rank0 + (int)blockIdx.y;
   if (r == kp.absent_rank) return;
   call_begin(kp, r);
@@ -1617,12 +1621,12 @@ __global__ void __launch_bounds__(32 * kNvlsWarps, 1) k_nvls(KParams kp) {
         nv_reduce_tile<OP>(kp, nv_tile(kp, kp.tile2_off[r] + b + G * k), lane_id);
       __syncwarp();
       // every reduction warp syncs too: a warp must not arrive twice at one barrier phase
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * (NW + 1)) : "memory");
     }
     stamp(kp, 2);  // (diagnostics) reduction warps done
   } else if (warp == NW) {
     for (int j = 0; j < nr; ++j) {
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * (NW + 1)) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * (NW + 1)) : "memory");
       if (lane_id == 0) {
         asm volatile("fence.acq_rel.sys;" ::: "memory");
         for (int q = 0; q < P; ++q)

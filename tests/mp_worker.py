@@ -131,14 +131,21 @@ def main():
     comm.set_tuning(0, 0, 0)
     comm.set_ll_max(0)
     with tc.Group(comm, views) as g:
-        for algo in algos:
+        # NVLS allreduce also on small CTAs (the comm's thread count: 2 and 4 warps, 1 and 3
+        # reducing) and a partial grid -- the launch shapes a co-running bucket uses (f1)
+        runs = [(a, c, t) for a in algos for c, t in ([(0, 0)] + ([(0, 128), (32, 64)]
+                                                                  if a == 4 else []))]
+        for algo, ctas, thr in runs:
             comm.set_algorithm(algo)
+            comm.set_tuning(ctas, thr, 0)
             for kind in ("int", "grad"):
                 xs = [W.group(numels, kind, 63, 0, k, W.GRAD) for k in range(p)]
                 for v, a in zip(views, xs[rank]):
                     v.copy_(torch.from_numpy(a))
                 tc.allreduce(g)
                 assert comm.last_launch()[0] == tc.tc.ALGO_NAMES[algo]
+                if algo == 4:
+                    assert comm.last_launch()[2] == (thr or 512), comm.last_launch()
                 got = to_host(views)
                 if algo != 4 or kind == "int":
                     assert_bitwise(got, O.allreduce(xs), f"sym allreduce algo {algo} {kind}")
@@ -154,6 +161,7 @@ def main():
                     hs = [torch.zeros_like(h) for _ in range(p)]
                     dist.all_gather(hs, h)
                     assert all(int(x) == int(hs[0]) for x in hs), "nvls ranks differ"
+        comm.set_tuning(0, 0, 0)
         if comm.multicast_supported:
             # fused SGD over NVLS: G within tolerance, epilogue bit-exact given G
             comm.set_algorithm(4)

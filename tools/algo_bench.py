@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--config", default="resnet50")
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0, help="register kernels / NVLS allreduce")
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -35,7 +36,7 @@ def main():
     numels = W.GROUPS[a.config]
     S = 4 * sum(numels)
     comm = tc.Comm.from_process_group(device=local)
-    comm.set_tuning(a.ctas, 0, -1)
+    comm.set_tuning(a.ctas, a.threads, -1)
     pristine = torch.from_numpy(np.concatenate(W.group(numels, "grad", 2, 0, rank, W.GRAD))).cuda()
     g_flat = comm.alloc_symmetric(sum(numels))
     g_flat.copy_(pristine)
@@ -73,7 +74,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             name, ctas, thr = comm.last_launch()
             if rank == 0:
-                print(json.dumps({"p": p, "op": op, "algo": name, "ctas": ctas, "median_us": t[0].item(),
+                print(json.dumps({"p": p, "op": op, "algo": name, "ctas": ctas, "threads": thr,
+                                  "median_us": t[0].item(),
                                   "mean_us": t[1].item(),
                                   "busbw_gbs": 2 * (p - 1) / p * S / t[1].item() / 1e3}), flush=True)
     for grp in (G, Wg, D, C):

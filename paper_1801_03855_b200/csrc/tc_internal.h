@@ -62,7 +62,12 @@ constexpr int kT2SmemCap = TC_T2_SMEM;
 #ifndef TC_T2_SMEM_SGD
 #define TC_T2_SMEM_SGD (160 * 1024)
 #endif
-constexpr int t2_cap(int op) { return op == 1 ? TC_T2_SMEM_SGD : kT2SmemCap; }
+#ifndef TC_T2_SMEM_EL
+#define TC_T2_SMEM_EL (192 * 1024)   // elastic ops (EASGD, fused elastic + SGD, async EASGD)
+#endif
+constexpr int t2_cap(int op) {
+  return op == 1 ? TC_T2_SMEM_SGD : (op == 2 || op == 3 || op == 5) ? TC_T2_SMEM_EL : kT2SmemCap;
+}
 constexpr int kT2MaxStages = 16;
 #ifndef TC_T2_CW
 #define TC_T2_CW 8

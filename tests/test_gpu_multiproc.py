@@ -40,3 +40,20 @@ def test_multiprocess_parity(p):
     sys.stderr.write(r.stderr[-4000:])
     assert r.returncode == 0
     assert f"MP_WORKER_OK p={p}" in r.stdout
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_multiprocess_stress(p):
+    """tools/stress_mp.py: 500 calls, every call changing the data, algorithms rotating (pull,
+    TMA, NVLS, one-shot, LL) with broadcasts interleaved; every call checked on the GPU."""
+    if NGPU < p:
+        pytest.skip(f"needs {p} GPUs, have {NGPU}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(os.path.dirname(HERE), "tools", "stress_mp.py"), "500"]
+    env = dict(os.environ, TC_TIMEOUT_MS="20000")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    sys.stdout.write(r.stdout[-2000:])
+    sys.stderr.write(r.stderr[-2000:])
+    assert r.returncode == 0
+    assert f"stress p={p} iters=500: mismatching calls 0, async errors 0" in r.stdout

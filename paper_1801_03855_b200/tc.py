@@ -440,8 +440,10 @@ class BucketedStep:
     tc_allreduce when w/dw are None.
     split (split=True): each bucket runs only tc_allreduce (link-bound, few SMs suffice:
     ``ctas``), and finish() runs the SGD update once over the whole group as a local HBM
-    stream (tc_sgd_step on a single-rank comm).  Bit-identical to the fused step: the allreduce
-    rounds the float64 sum once and the local step's "sum" of one rank is that value.
+    stream (tc_sgd_step on a single-rank comm).  Bit-identical to the fused step on the P2P
+    algorithms: the allreduce rounds the float64 sum once and the local step's "sum" of one rank
+    is that value.  (With switch reduction -- NVLS, tc_comm_set_switch_reduction / algorithm 4 --
+    both are within the NVLS tolerance instead, and identical on every rank.)
     """
 
     # defaults from bench_overlap.py on B200 (DESIGN.md §10): two large buckets and a 64-CTA

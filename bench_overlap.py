@@ -246,9 +246,9 @@ def main():
               else ((False, 0), (False, 64), (False, 32), (True, 0), (True, 64), (True, 32)))
     for split, ctas in shapes:
         side = cstream
-        if side is None and a.priority:
+        if side is None:  # explicit either way (BucketedStep's default is the highest priority)
             lo, hi = torch.cuda.Stream.priority_range()
-            side = torch.cuda.Stream(priority=hi)
+            side = torch.cuda.Stream(priority=hi if a.priority else lo)
         step = tc.BucketedStep(comm, g, w, dw, bucket_bytes=int(a.bucket_mb * (1 << 20)), ctas=ctas,
                                split=split, stream=side)
         # GEMM mode: cuBLAS leaves `ctas` SMs to the collective (SM carveout), as a framework

@@ -17,8 +17,8 @@ gradient buffer, so libtc groups wrap the model's own tensors (no copies):
   compute  -- forward + backward alone (no step), the floor.
 With --graph each mode's iteration is captured once as a CUDA graph (the bucket launches become
 side-stream nodes hanging off the gradient-producing kernels) and replayed, so host launch cost
-does not decide the comparison.  Per-iteration device time (CUDA events, max over ranks); hidden fraction = (serial - overlap) /
-(serial - compute).  After the timed iterations every rank's weights are compared (bitwise hash
+does not decide the comparison.  Per-iteration device time (CUDA events, max over ranks); hidden
+fraction = (serial - overlap) / (serial - compute) per round, median over rounds.  After the timed iterations every rank's weights are compared (bitwise hash
 allgather): the fused step keeps the replicas identical.  Rank 0 prints one JSON line per mode.
 """
 import argparse
@@ -106,7 +106,8 @@ def main():
     hp = dict(lr=0.1, momentum=0.9, wd=1e-4, rescale=1.0 / (world * a.batch))
     step = tc.BucketedStep(comm, gv, wv, dv, bucket_bytes=int(a.bucket_mb * (1 << 20)),
                            ctas=a.ctas, split=a.split,
-                           stream=torch.cuda.Stream(priority=-1) if a.priority else None)
+                           stream=torch.cuda.Stream(
+                               priority=torch.cuda.Stream.priority_range()[1] if a.priority else 0))
     # a hook on every parameter: the bucket launches when its last gradient is counted (hooking
     # only the lowest-index tensor of each bucket is NOT safe -- autograd may accumulate a
     # layer's weight before its bias, so a bucket could launch before its last gradient lands;
@@ -210,7 +211,12 @@ def main():
             "algo": comm.last_launch()[0],
             "t_compute_us": t_compute, "t_serial_us": t_serial,
             "t_overlap_us": t_overlap, "t_step_alone_us": t_step,
-            "hidden_fraction": (t_serial - t_overlap) / max(t_serial - t_compute, 1e-9),
+            # per round (the modes of one round ran back to back, so clock / power drift between
+            # rounds cancels), then the median over rounds
+            "hidden_fraction": sorted(
+                (s - o) / max(s - c, 1e-9) for c, s, o in
+                zip(runs["compute"], runs["serial"], runs["overlap"]))[len(runs["compute"]) // 2],
+            "hidden_fraction_of_medians": (t_serial - t_overlap) / max(t_serial - t_compute, 1e-9),
             "rounds": {k: [round(x, 1) for x in v] for k, v in runs.items()},
             "side_stream_priority": a.priority,
             "speedup_vs_serial": t_serial / t_overlap, "replicas_identical": same,

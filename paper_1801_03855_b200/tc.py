@@ -446,16 +446,18 @@ class BucketedStep:
     both are within the NVLS tolerance instead, and identical on every rank.)
     """
 
-    # defaults from bench_overlap.py on B200 (DESIGN.md §10): two large buckets and a 64-CTA
-    # collective hid 13% of the step at p = 4; 25 MiB buckets and the full grid hid none
-    def __init__(self, comm, g, w=None, dw=None, bucket_bytes=64 << 20, stream=None, ctas=64,
+    # defaults from a graph-captured ResNet-50 backward on B200 (bench_train.py, DESIGN.md §10):
+    # 25 MiB buckets, a 48-CTA budget and a highest-priority side stream hid 0.44 / 0.49 of the
+    # step at p = 4 with 8 / 4 images per GPU (the full grid hid none: the buckets then take SMs
+    # the backward's next kernels need)
+    def __init__(self, comm, g, w=None, dw=None, bucket_bytes=25 << 20, stream=None, ctas=48,
                  split=False):
         import torch
         numels = [t.numel() for t in (g[0] if comm.is_emulated else g)]
         plan = Plan(numels)
         self.bucket_of, self.nbuckets = plan.buckets(bucket_bytes)
         self.comm = comm
-        self.stream = stream or torch.cuda.Stream()
+        self.stream = stream or torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
         members = [[] for _ in range(self.nbuckets)]
         for t in range(len(numels)):
             members[self.bucket_of[t]].append(t)

@@ -4,6 +4,7 @@ allreduce + SGD-momentum update (libtc) overlaps the backward computation bucket
 
     torchrun --nproc-per-node N bench_train.py [--batch 64] [--iters 20] [--bucket-mb 25]
                                                [--graph] [--channels-last] [--split] [--ctas K]
+    where f1 pays: --graph --channels-last --batch 8 --ctas 48 --priority (p = 4)
 
 PAPER.md:59: gradients "are obtained as soon as a backward step for a layer is computed, these can
 be aggregated in parallel with the backward phase".  The model is torchvision's ResNet-50 (random
